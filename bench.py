@@ -1,0 +1,360 @@
+"""Benchmark: RQMC paths/s of the fused B200 path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c3|c5|c1] [--generator NAME]
+
+A step is one full run of the workload's replication loop on this rank
+(default C2: LIBOR caplet, 20 quarterly forwards, rasrap-recursive,
+M = 1024 replications x N = 2^20 paths): device randomisation setup, fused
+generator -> inverse normal -> Euler path -> payoff kernel, numpy-order
+reduction to theta.  Multi-GPU (torchrun, one process per GPU, NCCL) is
+weak scaling: every rank owns its own M replications (ids offset by rank),
+no data-path collective, theta all-gathered once per step; the time is the
+max over ranks.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (a bit-exact C restatement of the
+reference numba path, oracle/; the reference itself is Python+numba and has
+no compiled artefact to run here) on the host cores with all threads, on a
+bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SEED = 20120224
+
+# SURVEY 8(d) frozen FP64-slot convention (W per path / per normal)
+def libor_slots(S: int) -> float:
+    return 7.5 * S * S + 53.5 * S + 3
+
+
+MBS_SLOTS = 97 * 360 - 2
+WORKLOADS = {
+    # name: (model, maturity, accrual, M, N, description)
+    "c1": ("libor", 5.0, 0.25, 16, 10_000, "C1 LIBOR caplet S=20 (T=5, delta=0.25), M=16 x N=10^4"),
+    "c2": ("libor", 5.0, 0.25, 1024, 2**20, "C2 LIBOR caplet S=20 (T=5, delta=0.25), M=1024 x N=2^20"),
+    "c3": ("mbs", None, None, 256, 10**6, "C3 MBS 360 months, M=256 x N=10^6"),
+    "c5": ("libor", 20.0, 0.25, 8192, 2**20, "C5 LIBOR caplet S=80 (T=20, delta=0.25), M=8192 x N=2^20"),
+}
+
+
+def build_model(kind, maturity, accrual):
+    from paper_1408_5526_b200 import models as M
+
+    if kind == "libor":
+        return M.LiborModel(M.LiborConfig(maturity=maturity, accrual=accrual))
+    return M.MbsModel()
+
+
+def slots_per_path(model) -> float:
+    return libor_slots(model.dim) if model.name == "libor" else MBS_SLOTS
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- ours
+def device_step(gen_id, model, seed, first, count, grid, theta, lib, C, _lib):
+    """One workload step through the C ABI with device-resident output."""
+    h = C.c_void_p()
+    st = _lib.stream_ptr()
+    _lib.check(lib.rq_sampler_create(C.byref(h), gen_id, model.dim, seed, first, count, st))
+    ms, keep = _lib.model_struct(model)
+    import numpy as np
+
+    g = np.ascontiguousarray(grid, dtype=np.int64)
+    n = C.c_int32(0)
+    _lib.check(lib.rq_estimate(h, C.byref(ms), g.ctypes.data_as(C.POINTER(C.c_int64)), g.size,
+                               theta.data_ptr(), C.byref(n), st))
+    return h, n.value + (1 if gen_id in (0, 1, 3, 4) else 0), keep
+
+
+def run_ours(args) -> dict:
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1408_5526_b200 import _lib
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    lib = _lib.lib()
+    kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
+    model = build_model(kind, mat, acc)
+    gen = args.generator
+    gen_id = _lib.GEN_IDS[gen]
+    grid = (N,)
+    first = 1 + rank * M  # weak scaling: each rank its own replication ids
+    theta = torch.empty((M, 1), dtype=torch.float64, device="cuda")
+    gathered = [torch.empty_like(theta) for _ in range(world)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_step():
+        h, n, keep = device_step(gen_id, model, SEED, first, M, grid, theta, lib, C, _lib)
+        if world > 1:
+            dist.all_gather(gathered, theta)
+        return h, n
+
+    peak, peak_ms = _lib.fp64_peak()
+    launches = 0
+    for _ in range(args.warmup):
+        h, _ = one_step()
+        torch.cuda.synchronize()
+        lib.rq_sampler_destroy(h)
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flushed between timed iterations
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        h, n = one_step()
+        b.record()
+        b.synchronize()
+        lib.rq_sampler_destroy(h)
+        launches += n
+        step_ms.append(a.elapsed_time(b))
+    clk = clocks.stop()
+    ms = float(np.mean(step_ms))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    paths = M * N * world
+    value = paths / (ms * 1e-3)
+
+    # kernel share: one extra (untimed) step with per-kernel CUDA events
+    _lib.stats_reset(timing=True)
+    h, _ = one_step()
+    torch.cuda.synchronize()
+    lib.rq_sampler_destroy(h)
+    ks = _lib.stats_get()
+    _lib.stats_reset(timing=False)
+    W = slots_per_path(model)
+    achieved = M * N * W / (ks["paths_ms"] * 1e-3)  # per GPU, slots/s
+
+    # end to end through the host API: host in, theta to host every step
+    e2e_ms = []
+    _lib.stats_reset(timing=False)
+    for k in range(max(1, min(args.steps, 3))):
+        barrier()
+        t0 = time.perf_counter()
+        estimate_replications(gen, model, SEED, first, M, grid)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    tr = _lib.stats_get()
+    ne = len(e2e_ms)
+    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = paths / (float(e2e_t.item()) * 1e-3)
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": "RQMC paths/sec (LIBOR caplet, MBS) at 1/2/4/8 B200; % FP64 pipe peak",
+            "value": value,
+            "unit": "paths/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seed 20120224, replication ids from 1, packaged 2012-02-24 "
+                    "Treasury curve)",
+            "config": {"workload": desc, "generator": gen, "M_per_gpu": M, "N": N,
+                       "model": kind, "dim": model.dim, "parallelism": f"replications x{world}",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "roofline": {
+                "bound": "fp64",
+                "kernel": "k_paths_* (fused generator + inverse normal + path + payoff)",
+                "achieved": achieved / 1e12,
+                "peak": peak / 1e12,
+                "unit": "Tslot/s (FP64 pipe slots, SURVEY 8(d) convention)",
+                "frac": achieved / peak,
+                "slots_per_path": W,
+                "peak_source": "measured on this GPU by rq_fp64_peak (DFMA probe, burst)",
+                "paths_kernel_share": ks["paths_ms"] / max(ks["paths_ms"] + ks["reduce_ms"]
+                                                           + ks["setup_ms"], 1e-9),
+                "kernel_ms": {"setup": ks["setup_ms"], "paths": ks["paths_ms"],
+                              "reduce": ks["reduce_ms"]},
+                "traffic": None,
+            },
+            "e2e": {"value": e2e_value, "unit": "paths/s",
+                    "h2d_bytes_per_step": tr["h2d"] // ne, "d2h_bytes_per_step": tr["d2h"] // ne,
+                    "api": "rq_run_replications (host in / theta to host)"},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(model, gen, N, args)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+# ---------------------------------------------------------------- reference arm
+def cpu_sample(model, gen, N, reps, threads):
+    from oracle import oracle as O
+
+    sob = None
+    if gen.startswith("sobol"):
+        from paper_1408_5526_b200.tables import sobol_directions
+
+        sob = sobol_directions(model.dim)
+    t0 = time.perf_counter()
+    O.run_replications(gen, model, SEED, 1, reps, (N,), threads=threads, sobol_v=sob)
+    return reps * N / (time.perf_counter() - t0)
+
+
+def cpu_baseline(model, gen, N, args) -> dict:
+    from oracle import oracle as O
+
+    cores = O.host_cores()
+    reps = max(2, cores) if model.name == "libor" and model.dim <= 20 else max(2, cores // 2)
+    n = N if model.dim <= 20 else max(8192, N // 16)
+    rate = cpu_sample(model, gen, n, reps, cores)
+    return {"value": rate, "unit": "paths/s", "cores": cores, "kind": "port",
+            "sample": f"{reps} replications x N={n} of the same workload ({gen}), "
+                      f"oracle/rqmc_oracle.c (bit-exact C restatement of the reference numba "
+                      f"path), {cores} threads"}
+
+
+def run_reference(args) -> dict | None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+
+    kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
+    model = build_model(kind, mat, acc)
+    cores = O.host_cores()
+    reps = max(2, cores)
+    n = N if model.dim <= 20 else max(8192, N // 16)
+    for _ in range(args.warmup):
+        cpu_sample(model, args.generator, 8192, 2, cores)
+    rates = [cpu_sample(model, args.generator, n, reps, cores) for _ in range(args.steps)]
+    v = float(statistics.median(rates))
+    samp = f"{reps} replications x N={n} per step, {args.generator}"
+    return {
+        "metric": "RQMC paths/sec (LIBOR caplet, MBS) at 1/2/4/8 B200; % FP64 pipe peak",
+        "impl": "reference",
+        "value": v,
+        "unit": "paths/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": reps * n / v * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seed 20120224)",
+        "config": {"workload": desc, "generator": args.generator, "M": M, "N": N},
+        "cpu_baseline": {"value": v, "unit": "paths/s", "cores": cores, "kind": "port",
+                         "sample": samp + " (oracle/rqmc_oracle.c, bit-exact restatement of "
+                                          "the reference numba kernels)"},
+        "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--generator", default="rasrap-recursive")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if out is not None:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

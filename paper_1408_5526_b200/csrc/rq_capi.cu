@@ -1,0 +1,737 @@
+// rq_capi.cu -- C ABI (include/rqmc_b200.h): host tables, device contexts,
+// batching of replications and numpy pairwise-sum plans.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rqmc_b200.h"
+#include "rq_device.cuh"
+#include "rq_internal.h"
+
+namespace {
+
+#include "joe_kuo_421.inc"
+
+thread_local std::string g_err;
+
+// host<->device byte counters and optional per-kernel timing (bench.py)
+struct Stats {
+  uint64_t h2d = 0, d2h = 0;
+  bool timing = false;
+  double paths_ms = 0, reduce_ms = 0, setup_ms = 0;
+  int64_t paths_launches = 0;
+} g_stats;
+std::mutex g_stats_mu;
+
+struct KTimer {  // CUDA events on the launching stream when timing is on
+  cudaEvent_t a = nullptr, b = nullptr;
+  double *acc;
+  cudaStream_t s;
+  KTimer(double *acc_, cudaStream_t s_) : acc(acc_), s(s_) {
+    if (g_stats.timing) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~KTimer() {
+    if (a) {
+      cudaEventRecord(b, s);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      *acc += ms;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  }
+};
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define RQ_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(RQ_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                             \
+  } while (0)
+
+// ------------------------------------------------------------------ Halton constants
+struct HostTables {
+  std::vector<rq::HaltonDim> dims;
+  std::vector<double> wts, cscale;
+  int total_bases(int dim) const { return dim ? dims[dim - 1].sig_off + dims[dim - 1].base : 0; }
+  int total_caps(int dim) const { return dim ? dims[dim - 1].dig_off + dims[dim - 1].cap : 0; }
+  int total_sums(int dim) const { return dim ? dims[dim - 1].sum_off + dims[dim - 1].cap + 1 : 0; }
+};
+
+// numba `float ** int` (int_power): r = 1; while e: if e & 1: r *= a; e >>= 1; a *= a
+double numba_ipow(double a, int64_t e) {
+  double r = 1.0;
+  while (e != 0) {
+    if (e & 1) r = rq::dmul(r, a);
+    e >>= 1;
+    a = rq::dmul(a, a);
+  }
+  return r;
+}
+
+const HostTables &host_tables() {
+  static HostTables T;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    std::vector<int> primes;
+    for (int c = 2; (int)primes.size() < rq::MAX_DIM; c++) {
+      bool ok = true;
+      for (int p : primes) {
+        if (p * p > c) break;
+        if (c % p == 0) {
+          ok = false;
+          break;
+        }
+      }
+      if (ok) primes.push_back(c);
+    }
+    int sig = 0, dig = 0, sum = 0;
+    for (int d = 0; d < rq::MAX_DIM; d++) {
+      rq::HaltonDim h{};
+      int p = primes[d];
+      h.base = p;
+      int K = 1;
+      unsigned __int128 v = p;
+      while (v < ((unsigned __int128)1 << 32)) {  // halton.py:59-66
+        v *= p;
+        K++;
+      }
+      h.K = K;
+      h.cap = K + 8;
+      int ell = 0;
+      while ((1 << ell) < p) ell++;
+      h.ell = ell;
+      unsigned __int128 num = ((unsigned __int128)1) << (32 + ell);
+      uint64_t m = (uint64_t)((num + p - 1) / p);  // ceil(2^(32+ell)/p) in [2^32, 2^33]
+      h.mlo = (uint32_t)m;
+      h.sig_off = sig;
+      h.dig_off = dig;
+      h.sum_off = sum;
+      h.inv_p = 1.0 / (double)p;
+      h.scale0 = std::pow(h.inv_p, (double)K);  // Python float ** int -> C pow
+      T.dims.push_back(h);
+      for (int j = 0; j < h.cap + 1; j++) T.wts.push_back(numba_ipow(h.inv_p, j + 1));
+      double s = 1.0;
+      for (int j = 0; j < h.cap + 1; j++) {
+        s = rq::dmul(s, h.inv_p);
+        T.cscale.push_back(s);
+      }
+      sig += p;
+      dig += h.cap;
+      sum += h.cap + 1;
+    }
+  });
+  return T;
+}
+
+int ensure_device_tables() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  RQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return RQ_OK;
+  // keep freed cudaMallocAsync memory in the pool across synchronisations
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  const HostTables &T = host_tables();
+  RQ_CUDA(rq::upload_halton_dims(T.dims.data(), (int)T.dims.size(), T.wts.data(),
+                                 T.cscale.data(), (int)T.wts.size()));
+  done.push_back(dev);
+  return RQ_OK;
+}
+
+// Joe-Kuo expansion: m-recursion (sobol.py:61-71), v_k = m_k << (32 - k).
+int sobol_v(int dim, uint32_t *v) {
+  if (dim < 1 || dim > kJoeKuoDims) return fail(RQ_ERR_VALUE, "sobol dim %d outside 1..%d", dim, kJoeKuoDims);
+  for (int k = 1; k <= 32; k++) v[k - 1] = 1u << (32 - k);  // dimension 1: m_k = 1
+  size_t pos = 0;
+  for (int d = 2; d <= dim; d++) {
+    int s = (int)kJoeKuoPacked[pos], a = (int)kJoeKuoPacked[pos + 1];
+    std::vector<uint64_t> m(kJoeKuoPacked + pos + 2, kJoeKuoPacked + pos + 2 + s);
+    pos += 2 + s;
+    for (int k = s; k < 32; k++) {
+      uint64_t acc = (m[k - s] << s) ^ m[k - s];
+      for (int i = 1; i < s; i++)
+        if ((a >> (s - 1 - i)) & 1) acc ^= m[k - i] << i;
+      m.push_back(acc);
+    }
+    for (int k = 1; k <= 32; k++) v[(d - 1) * 32 + k - 1] = (uint32_t)(m[k - 1] << (32 - k));
+  }
+  return RQ_OK;
+}
+
+// ------------------------------------------------------------------ pairwise plan
+struct HostPlan {
+  int64_t n;
+  std::vector<int64_t> leaf_start;
+  std::vector<int32_t> leaf_len;
+  std::vector<int32_t> level_off, node_id, node_l, node_r;
+  int32_t root, nnodes;
+};
+
+// numpy pairwise_sum recursion: n <= 128 leaf, else split at
+// n2 = n/2 - (n/2 % 8).  Leaves get ids 0..L-1 in order; internal nodes
+// ids >= L grouped by height so each level only depends on lower ones.
+void build_plan(int64_t n, HostPlan &P) {
+  P.n = n;
+  struct Frame {
+    int64_t start, len;
+    int state;
+  };
+  // iterative post-order walk; provisional ids: leaf k -> k, internal k -> -(k+1)
+  std::vector<Frame> st;
+  std::vector<int32_t> out_stack;
+  std::vector<std::pair<int32_t, int32_t>> children;
+  std::vector<int32_t> int_height;
+  auto height = [&](int32_t id) { return id >= 0 ? 0 : int_height[-id - 1]; };
+  st.push_back({0, n, 0});
+  while (!st.empty()) {
+    Frame &f = st.back();
+    if (f.len <= 128) {
+      P.leaf_start.push_back(f.start);
+      P.leaf_len.push_back((int32_t)f.len);
+      out_stack.push_back((int32_t)P.leaf_start.size() - 1);
+      st.pop_back();
+      continue;
+    }
+    int64_t n2 = f.len / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st.push_back({f.start, n2, 0});
+    } else if (f.state == 1) {
+      f.state = 2;
+      Frame c{f.start + n2, f.len - n2, 0};
+      st.push_back(c);
+    } else {
+      int32_t r = out_stack.back();
+      out_stack.pop_back();
+      int32_t l = out_stack.back();
+      out_stack.pop_back();
+      children.push_back({l, r});
+      int_height.push_back(std::max(height(l), height(r)) + 1);
+      out_stack.push_back(-(int32_t)children.size());
+      st.pop_back();
+    }
+  }
+  int32_t L = (int32_t)P.leaf_len.size();
+  int32_t I = (int32_t)children.size();
+  auto fin = [&](int32_t id) { return id >= 0 ? id : L + (-id - 1); };
+  int32_t H = 0;
+  for (int32_t h : int_height) H = std::max(H, h);
+  P.level_off.assign(H + 1, 0);
+  std::vector<std::vector<int32_t>> by_h(H + 1);
+  for (int32_t k = 0; k < I; k++) by_h[int_height[k]].push_back(k);
+  for (int32_t h = 1; h <= H; h++) {
+    P.level_off[h - 1] = (int32_t)P.node_id.size();
+    for (int32_t k : by_h[h]) {
+      P.node_id.push_back(L + k);
+      P.node_l.push_back(fin(children[k].first));
+      P.node_r.push_back(fin(children[k].second));
+    }
+  }
+  if (H >= 1) P.level_off[H] = (int32_t)P.node_id.size();
+  P.level_off.resize(H + 1);
+  P.root = fin(out_stack.back());
+  P.nnodes = L + I;
+}
+
+struct DevPlan {
+  rq::SumPlan p{};
+  void *buf = nullptr;
+};
+
+int upload_plan(const HostPlan &hp, DevPlan &dp, cudaStream_t s) {
+  size_t nl = hp.leaf_start.size(), ni = hp.node_id.size(), nlev = hp.level_off.size();
+  size_t bytes = nl * 8 + nl * 4 + nlev * 4 + 3 * ni * 4 + 64;
+  RQ_CUDA(cudaMallocAsync(&dp.buf, bytes, s));
+  char *b = (char *)dp.buf;
+  std::vector<char> host(bytes);
+  size_t off = 0;
+  auto put = [&](const void *src, size_t n) {
+    std::memcpy(host.data() + off, src, n);
+    char *dst = b + off;
+    off += (n + 7) & ~(size_t)7;
+    return dst;
+  };
+  dp.p.n = hp.n;
+  dp.p.nleaves = (int32_t)nl;
+  dp.p.nnodes = hp.nnodes;
+  dp.p.nlevels = (int32_t)nlev - 1 > 0 ? (int32_t)nlev - 1 : 0;
+  dp.p.root = hp.root;
+  dp.p.leaf_start = (const int64_t *)put(hp.leaf_start.data(), nl * 8);
+  dp.p.leaf_len = (const int32_t *)put(hp.leaf_len.data(), nl * 4);
+  dp.p.level_off = (const int32_t *)put(hp.level_off.data(), nlev * 4);
+  dp.p.node_id = (const int32_t *)put(hp.node_id.data(), ni * 4);
+  dp.p.node_l = (const int32_t *)put(hp.node_l.data(), ni * 4);
+  dp.p.node_r = (const int32_t *)put(hp.node_r.data(), ni * 4);
+  RQ_CUDA(cudaMemcpyAsync(dp.buf, host.data(), off, cudaMemcpyHostToDevice, s));
+  g_stats.h2d += off;
+  // the host staging buffer must outlive the copy
+  RQ_CUDA(cudaStreamSynchronize(s));
+  return RQ_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ sampler
+struct rq_sampler {
+  rq::RepTables t{};
+  void *mem = nullptr;
+  bool owns = true;
+};
+
+extern "C" {
+
+const char *rq_last_error(void) { return g_err.c_str(); }
+int rq_abi_version(void) { return RQ_ABI_VERSION; }
+
+int rq_sobol_directions(int dim, uint32_t *v_host) { return sobol_v(dim, v_host); }
+
+int rq_halton_constants(int dim, int32_t *base, int32_t *K, double *scale0) {
+  if (dim < 1 || dim > rq::MAX_DIM) return fail(RQ_ERR_VALUE, "dim %d outside 1..%d", dim, rq::MAX_DIM);
+  const HostTables &T = host_tables();
+  for (int d = 0; d < dim; d++) {
+    if (base) base[d] = T.dims[d].base;
+    if (K) K[d] = T.dims[d].K;
+    if (scale0) scale0[d] = T.dims[d].scale0;
+  }
+  return RQ_OK;
+}
+
+int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
+                      int64_t rep_first, int32_t rep_count, void *stream) {
+  if (!out) return fail(RQ_ERR_VALUE, "out is NULL");
+  *out = nullptr;
+  if (generator < 0 || generator > rq::GEN_SFC64)
+    return fail(RQ_ERR_VALUE, "unknown generator id %d", generator);
+  if (dim < 1) return fail(RQ_ERR_VALUE, "dimension must be >= 1");
+  if (rep_count < 1) return fail(RQ_ERR_VALUE, "rep_count must be >= 1");
+  bool rasrap = generator == rq::GEN_RASRAP_RECURSIVE || generator == rq::GEN_RASRAP_COUNTER;
+  bool sob = generator == rq::GEN_SOBOL_GRAY || generator == rq::GEN_SOBOL_COUNTER;
+  if (rasrap && dim > rq::MAX_DIM)
+    return fail(RQ_ERR_VALUE, "rasrap dimension %d exceeds %d", dim, rq::MAX_DIM);
+  if (sob && dim > kJoeKuoDims)
+    return fail(RQ_ERR_VALUE, "source provides %d dimensions, %d requested", kJoeKuoDims, dim);
+  int rc = ensure_device_tables();
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  rq_sampler *S = new rq_sampler();
+  rq::RepTables &t = S->t;
+  t.gen = generator;
+  t.dim = dim;
+  t.seed = seed;
+  t.rep_first = rep_first;
+  t.rep_count = rep_count;
+  const HostTables &T = host_tables();
+  if (rasrap) {
+    t.sig_stride = T.total_bases(dim);
+    t.dig_stride = (T.total_caps(dim) + 3) & ~3;
+    t.sum_stride = T.total_sums(dim);
+    size_t b_sig = sizeof(double) * t.sig_stride * rep_count;
+    size_t b_sum = sizeof(double) * t.sum_stride * rep_count;
+    size_t b_dig = sizeof(uint16_t) * t.dig_stride * rep_count;
+    cudaError_t e = cudaMallocAsync(&S->mem, b_sig + b_sum + b_dig, s);
+    if (e != cudaSuccess) {
+      delete S;
+      return fail(RQ_ERR_CUDA, "allocating rasrap tables (%zu B): %s", b_sig + b_sum + b_dig,
+                  cudaGetErrorString(e));
+    }
+    double *sig = (double *)S->mem;
+    double *sums = sig + t.sig_stride * rep_count;
+    uint16_t *dig = (uint16_t *)(sums + t.sum_stride * rep_count);
+    t.sigma = sig;
+    t.sums = sums;
+    t.digits = dig;
+    {
+      KTimer kt(&g_stats.setup_ms, s);
+      e = rq::launch_rasrap_setup(t, sig, dig, sums, s);
+    }
+    if (e != cudaSuccess) {
+      cudaFreeAsync(S->mem, s);
+      delete S;
+      return fail(RQ_ERR_CUDA, "rasrap setup: %s", cudaGetErrorString(e));
+    }
+  } else if (sob) {
+    std::vector<uint32_t> v((size_t)dim * 32);
+    if ((rc = sobol_v(dim, v.data()))) {
+      delete S;
+      return rc;
+    }
+    size_t b_v = sizeof(uint32_t) * dim * 32;
+    size_t b_gen = b_v * rep_count, b_sh = sizeof(uint32_t) * dim * rep_count;
+    cudaError_t e = cudaMallocAsync(&S->mem, b_v + b_gen + b_sh, s);
+    if (e != cudaSuccess) {
+      delete S;
+      return fail(RQ_ERR_CUDA, "allocating sobol tables: %s", cudaGetErrorString(e));
+    }
+    uint32_t *vd = (uint32_t *)S->mem;
+    uint32_t *gen = vd + (size_t)dim * 32;
+    uint32_t *sh = gen + (size_t)dim * 32 * rep_count;
+    e = cudaMemcpyAsync(vd, v.data(), b_v, cudaMemcpyHostToDevice, s);
+    g_stats.h2d += b_v;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // v is a host temporary
+    if (e == cudaSuccess) {
+      KTimer kt(&g_stats.setup_ms, s);
+      e = rq::launch_sobol_setup(t, vd, gen, sh, s);
+    }
+    if (e != cudaSuccess) {
+      cudaFreeAsync(S->mem, s);
+      delete S;
+      return fail(RQ_ERR_CUDA, "sobol setup: %s", cudaGetErrorString(e));
+    }
+    t.sobol_v = gen;
+    t.sobol_shift = sh;
+  }
+  *out = S;
+  return RQ_OK;
+}
+
+void rq_sampler_destroy(rq_sampler *s) {
+  if (!s) return;
+  if (s->mem) cudaFree(s->mem);
+  delete s;
+}
+
+static int check_rep(rq_sampler *s, int32_t rl) {
+  if (!s) return fail(RQ_ERR_VALUE, "sampler is NULL");
+  if (rl < 0 || rl >= s->t.rep_count)
+    return fail(RQ_ERR_VALUE, "replication %d outside the sampler's %d", rl, s->t.rep_count);
+  return RQ_OK;
+}
+
+int rq_sampler_points(rq_sampler *s, int32_t rep_local, int64_t first, int64_t count,
+                      double *out_dev, void *stream) {
+  int rc = check_rep(s, rep_local);
+  if (rc) return rc;
+  if (first < 0 || count < 0) return fail(RQ_ERR_VALUE, "index must be non-negative");
+  if (first + count > (int64_t)1 << 32)
+    return fail(RQ_ERR_RANGE, "point index %lld exceeds 2^32", (long long)(first + count));
+  if (count == 0) return RQ_OK;
+  RQ_CUDA(rq::launch_points(s->t, rep_local, first, nullptr, count, out_dev, (cudaStream_t)stream));
+  return RQ_OK;
+}
+
+int rq_sampler_points_at(rq_sampler *s, int32_t rep_local, const int64_t *idx_dev,
+                         int64_t count, double *out_dev, void *stream) {
+  int rc = check_rep(s, rep_local);
+  if (rc) return rc;
+  if (count <= 0) return count < 0 ? fail(RQ_ERR_VALUE, "count < 0") : RQ_OK;
+  RQ_CUDA(rq::launch_points(s->t, rep_local, 0, idx_dev, count, out_dev, (cudaStream_t)stream));
+  return RQ_OK;
+}
+
+int rq_sampler_rasrap_tables(rq_sampler *s, int32_t rep_local, uint16_t *digits_host,
+                             double *sigma_host, double *sums_host) {
+  int rc = check_rep(s, rep_local);
+  if (rc) return rc;
+  const rq::RepTables &t = s->t;
+  if (t.gen != rq::GEN_RASRAP_RECURSIVE && t.gen != rq::GEN_RASRAP_COUNTER)
+    return fail(RQ_ERR_VALUE, "not a rasrap sampler");
+  RQ_CUDA(cudaDeviceSynchronize());
+  if (digits_host)
+    RQ_CUDA(cudaMemcpy(digits_host, t.digits + rep_local * t.dig_stride,
+                       sizeof(uint16_t) * t.dig_stride, cudaMemcpyDeviceToHost));
+  if (sigma_host)
+    RQ_CUDA(cudaMemcpy(sigma_host, t.sigma + rep_local * t.sig_stride,
+                       sizeof(double) * t.sig_stride, cudaMemcpyDeviceToHost));
+  if (sums_host)
+    RQ_CUDA(cudaMemcpy(sums_host, t.sums + rep_local * t.sum_stride,
+                       sizeof(double) * t.sum_stride, cudaMemcpyDeviceToHost));
+  return RQ_OK;
+}
+
+static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, double **tab_dev,
+                           cudaStream_t s) {
+  if (!m) return fail(RQ_ERR_VALUE, "model is NULL");
+  if (m->kind < 0 || m->kind > rq::MODEL_CONST1) return fail(RQ_ERR_VALUE, "unknown model kind %d", m->kind);
+  if (m->dim != dim) return fail(RQ_ERR_VALUE, "model dim %d != sampler dim %d", m->dim, dim);
+  if (m->kind == rq::MODEL_LIBOR && !(m->dim == 10 || m->dim == 20 || m->dim == 40 || m->dim == 80))
+    return fail(RQ_ERR_VALUE, "LIBOR steps %d not compiled (10, 20, 40, 80)", m->dim);
+  mp.kind = m->kind;
+  mp.dim = m->dim;
+  mp.delta = m->delta;
+  mp.sigma = m->sigma;
+  mp.strike = m->strike;
+  mp.front_factor = m->front_factor;
+  mp.i0 = m->i0;
+  mp.k0 = m->k0;
+  mp.k1 = m->k1;
+  mp.k2 = m->k2;
+  mp.k3 = m->k3;
+  mp.k4 = m->k4;
+  mp.sigma_xi = m->sigma_xi;
+  mp.payment = m->payment;
+  mp.table = nullptr;
+  *tab_dev = nullptr;
+  if (m->kind == rq::MODEL_LIBOR || m->kind == rq::MODEL_MBS) {
+    if (!m->table) return fail(RQ_ERR_VALUE, "model table is NULL");
+    RQ_CUDA(cudaMallocAsync((void **)tab_dev, sizeof(double) * m->dim, s));
+    RQ_CUDA(cudaMemcpyAsync(*tab_dev, m->table, sizeof(double) * m->dim, cudaMemcpyHostToDevice, s));
+    g_stats.h2d += sizeof(double) * m->dim;
+    mp.table = *tab_dev;
+  }
+  return RQ_OK;
+}
+
+static int check_grid(const int64_t *grid, int32_t ngrid) {
+  if (!grid || ngrid < 1) return fail(RQ_ERR_VALUE, "n_grid must be a nonempty list of positive sizes");
+  for (int g = 0; g < ngrid; g++) {
+    if (grid[g] < 1) return fail(RQ_ERR_VALUE, "n_grid must be a nonempty list of positive sizes");
+    if (g && grid[g] <= grid[g - 1]) return fail(RQ_ERR_VALUE, "n_grid must be strictly increasing");
+  }
+  if (grid[ngrid - 1] > ((int64_t)1 << 32)) return fail(RQ_ERR_RANGE, "N exceeds 2^32 paths");
+  return RQ_OK;
+}
+
+int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, int32_t ngrid,
+                double *theta_dev, int32_t *kernel_launches, void *stream) {
+  if (!s) return fail(RQ_ERR_VALUE, "sampler is NULL");
+  int rc = check_grid(grid_host, ngrid);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  rq::ModelParams mp;
+  double *tab = nullptr;
+  if ((rc = model_to_params(model, s->t.dim, mp, &tab, st))) return rc;
+  const int64_t nmax = grid_host[ngrid - 1];
+  // replication batch: payoff buffer <= 256 MiB, >= 1 replication
+  int64_t B = std::max<int64_t>(1, ((int64_t)32 << 20) / nmax);
+  B = std::min<int64_t>(B, s->t.rep_count);
+  std::vector<HostPlan> hplans(ngrid);
+  std::vector<DevPlan> dplans(ngrid);
+  int32_t maxnodes = 1;
+  for (int g = 0; g < ngrid; g++) {
+    build_plan(grid_host[g], hplans[g]);
+    maxnodes = std::max(maxnodes, hplans[g].nnodes);
+    if ((rc = upload_plan(hplans[g], dplans[g], st))) return rc;
+  }
+  double *pay = nullptr, *scratch = nullptr;
+  unsigned *tickets = nullptr;
+  RQ_CUDA(cudaMallocAsync((void **)&pay, sizeof(double) * B * nmax, st));
+  RQ_CUDA(cudaMallocAsync((void **)&scratch, sizeof(double) * B * maxnodes, st));
+  RQ_CUDA(cudaMallocAsync((void **)&tickets, sizeof(unsigned) * B, st));
+  RQ_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * B, st));
+  int launched = 0;
+  for (int64_t r0 = 0; r0 < s->t.rep_count; r0 += B) {
+    int rn = (int)std::min<int64_t>(B, s->t.rep_count - r0);
+    cudaError_t e;
+    {
+      KTimer kt(&g_stats.paths_ms, st);
+      e = rq::launch_paths(s->t, mp, (int)r0, rn, nmax, pay, &launched, st);
+      g_stats.paths_launches++;
+    }
+    if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "path kernel: %s", cudaGetErrorString(e));
+    for (int g = 0; g < ngrid; g++) {
+      KTimer kt(&g_stats.reduce_ms, st);
+      e = rq::launch_reduce(dplans[g].p, pay, nmax, rn, theta_dev + r0 * ngrid + g, ngrid,
+                            scratch, tickets, st);
+      if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "reduce kernel: %s", cudaGetErrorString(e));
+      launched++;
+    }
+  }
+  cudaFreeAsync(pay, st);
+  cudaFreeAsync(scratch, st);
+  cudaFreeAsync(tickets, st);
+  if (tab) cudaFreeAsync(tab, st);
+  for (auto &d : dplans) cudaFreeAsync(d.buf, st);
+  if (kernel_launches) *kernel_launches += launched;
+  return RQ_OK;
+}
+
+int rq_run_replications(int generator, const rq_model *model, uint64_t seed, int64_t rep_first,
+                        int64_t rep_count, const int64_t *grid_host, int32_t ngrid,
+                        double *theta_host, int32_t *kernel_launches) {
+  if (!theta_host) return fail(RQ_ERR_VALUE, "theta_host is NULL");
+  if (rep_count < 1) return fail(RQ_ERR_VALUE, "need at least one replication");
+  int rc = check_grid(grid_host, ngrid);
+  if (rc) return rc;
+  static cudaStream_t st = nullptr;
+  if (!st) RQ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double *theta_dev = nullptr;
+  RQ_CUDA(cudaMallocAsync((void **)&theta_dev, sizeof(double) * rep_count * ngrid, st));
+  // replication groups bound the randomisation tables (<= ~256 MiB)
+  const int64_t G = 4096;
+  for (int64_t r0 = 0; r0 < rep_count; r0 += G) {
+    int32_t rn = (int32_t)std::min<int64_t>(G, rep_count - r0);
+    rq_sampler *S = nullptr;
+    if ((rc = rq_sampler_create(&S, generator, model ? model->dim : 0, seed, rep_first + r0, rn, st)))
+      return rc;
+    if (kernel_launches && generator != rq::GEN_PHILOX && generator != rq::GEN_SFC64)
+      *kernel_launches += 1;
+    rc = rq_estimate(S, model, grid_host, ngrid, theta_dev + r0 * ngrid, kernel_launches, st);
+    RQ_CUDA(cudaStreamSynchronize(st));
+    rq_sampler_destroy(S);
+    if (rc) return rc;
+  }
+  RQ_CUDA(cudaMemcpyAsync(theta_host, theta_dev, sizeof(double) * rep_count * ngrid,
+                          cudaMemcpyDeviceToHost, st));
+  g_stats.d2h += sizeof(double) * rep_count * ngrid;
+  RQ_CUDA(cudaFreeAsync(theta_dev, st));
+  RQ_CUDA(cudaStreamSynchronize(st));
+  for (int64_t k = 0; k < rep_count * ngrid; k++)
+    if (!std::isfinite(theta_host[k]))
+      return fail(RQ_ERR_NONFINITE, "replication %lld produced a non-finite estimate",
+                  (long long)(rep_first + k / ngrid));
+  return RQ_OK;
+}
+
+int rq_model_payoffs(const rq_model *model, const double *u_dev, int64_t npaths,
+                     double *out_dev, void *stream) {
+  if (!model) return fail(RQ_ERR_VALUE, "model is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  rq::ModelParams mp;
+  double *tab = nullptr;
+  int rc = model_to_params(model, model->dim, mp, &tab, st);
+  if (rc) return rc;
+  if (mp.kind != rq::MODEL_LIBOR && mp.kind != rq::MODEL_MBS)
+    return fail(RQ_ERR_VALUE, "payoff kernel only for libor/mbs");
+  RQ_CUDA(rq::launch_model_payoffs(mp, u_dev, npaths, out_dev, st));
+  if (tab) cudaFreeAsync(tab, st);
+  return RQ_OK;
+}
+
+int rq_inv_normal(const double *u_dev, int64_t n, double *out_dev, void *stream) {
+  RQ_CUDA(rq::launch_inv_normal(u_dev, n, out_dev, (cudaStream_t)stream));
+  return RQ_OK;
+}
+
+int rq_stream_normals(rq_sampler *s, int32_t rep_local, int64_t npoints, double *sum_dev,
+                      double *store_dev, void *stream) {
+  int rc = check_rep(s, rep_local);
+  if (rc) return rc;
+  if (npoints < 1 || npoints > ((int64_t)1 << 32)) return fail(RQ_ERR_VALUE, "npoints outside 1..2^32");
+  cudaStream_t st = (cudaStream_t)stream;
+  int blocks = rq::paths_grid_blocks(s->t, rq::ModelParams{rq::MODEL_X1, s->t.dim});
+  double *bs = nullptr;
+  RQ_CUDA(cudaMallocAsync((void **)&bs, sizeof(double) * blocks, st));
+  RQ_CUDA(rq::launch_stream_normals(s->t, rep_local, npoints, bs, blocks, store_dev, st));
+  rc = rq_pairwise_sum(bs, blocks, sum_dev, stream);
+  cudaFreeAsync(bs, st);
+  return rc;
+}
+
+void rq_stats_reset(int timing) {
+  g_stats = Stats();
+  g_stats.timing = timing != 0;
+}
+
+void rq_stats_get(uint64_t *h2d, uint64_t *d2h, double *setup_ms, double *paths_ms,
+                  double *reduce_ms, int64_t *paths_launches) {
+  if (h2d) *h2d = g_stats.h2d;
+  if (d2h) *d2h = g_stats.d2h;
+  if (setup_ms) *setup_ms = g_stats.setup_ms;
+  if (paths_ms) *paths_ms = g_stats.paths_ms;
+  if (reduce_ms) *reduce_ms = g_stats.reduce_ms;
+  if (paths_launches) *paths_launches = g_stats.paths_launches;
+}
+
+int rq_fp64_peak(double *slots_per_s, double *ms_out) {
+  int dev = 0, sms = 0;
+  RQ_CUDA(cudaGetDevice(&dev));
+  RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double *sink = nullptr;
+  RQ_CUDA(cudaMalloc(&sink, 256 * sizeof(double)));
+  cudaEvent_t a, b;
+  RQ_CUDA(cudaEventCreate(&a));
+  RQ_CUDA(cudaEventCreate(&b));
+  const int blocks = sms * 8, iters = 4096;
+  RQ_CUDA(rq::launch_dfma_peak(blocks, 64, sink, 0));  // warm-up / clocks up
+  RQ_CUDA(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 5; r++) {
+    RQ_CUDA(cudaEventRecord(a, 0));
+    RQ_CUDA(rq::launch_dfma_peak(blocks, iters, sink, 0));
+    RQ_CUDA(cudaEventRecord(b, 0));
+    RQ_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    RQ_CUDA(cudaEventElapsedTime(&ms, a, b));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  double slots = (double)blocks * 256 * iters * rq::PEAK_SLOTS_PER_ITER;
+  if (slots_per_s) *slots_per_s = slots / (best * 1e-3);
+  if (ms_out) *ms_out = best;
+  return RQ_OK;
+}
+
+int rq_pairwise_sum_host(const double *a_host, int64_t n, double *out_host) {
+  if (n < 1 || !a_host || !out_host) return fail(RQ_ERR_VALUE, "n must be >= 1");
+  HostPlan hp;
+  build_plan(n, hp);
+  std::vector<double> val(hp.nnodes);
+  for (size_t k = 0; k < hp.leaf_len.size(); k++) {
+    const double *a = a_host + hp.leaf_start[k];
+    int m = hp.leaf_len[k];
+    double res = 0.0;
+    if (m < 8) {
+      for (int i = 0; i < m; i++) res += a[i];
+    } else {
+      double r[8];
+      int i;
+      for (int j = 0; j < 8; j++) r[j] = a[j];
+      for (i = 8; i < m - (m % 8); i += 8)
+        for (int j = 0; j < 8; j++) r[j] += a[i + j];
+      res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      for (; i < m; i++) res += a[i];
+    }
+    val[k] = res;
+  }
+  for (size_t lv = 0; lv + 1 < hp.level_off.size(); lv++)
+    for (int32_t e = hp.level_off[lv]; e < hp.level_off[lv + 1]; e++)
+      val[hp.node_id[e]] = val[hp.node_l[e]] + val[hp.node_r[e]];
+  *out_host = val[hp.root];
+  return RQ_OK;
+}
+
+int rq_pairwise_sum(const double *a_dev, int64_t n, double *out_dev, void *stream) {
+  if (n < 1) return fail(RQ_ERR_VALUE, "n must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  HostPlan hp;
+  build_plan(n, hp);
+  DevPlan dp;
+  int rc = upload_plan(hp, dp, st);
+  if (rc) return rc;
+  double *scratch = nullptr;
+  unsigned *tickets = nullptr;
+  RQ_CUDA(cudaMallocAsync((void **)&scratch, sizeof(double) * hp.nnodes, st));
+  RQ_CUDA(cudaMallocAsync((void **)&tickets, sizeof(unsigned), st));
+  RQ_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned), st));
+  // theta = sum / n: multiply back by n is not exact, so reduce with n = 1 divisor
+  dp.p.n = 1;
+  RQ_CUDA(rq::launch_reduce(dp.p, a_dev, n, 1, out_dev, 1, scratch, tickets, st));
+  cudaFreeAsync(scratch, st);
+  cudaFreeAsync(tickets, st);
+  cudaFreeAsync(dp.buf, st);
+  return RQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+// rq_device.cuh -- host/device building blocks of the B200 RQMC path.
+//
+// Everything here is compiled both for sm_100a (kernels) and for the host
+// (table builders in rq_capi.cu), so the device and host table paths share
+// one definition.  Bit-exact pieces (Halton chains) use __dadd_rn /
+// __dmul_rn explicitly so nvcc can never contract them into FMAs.
+#pragma once
+#include <cstdint>
+#include <cmath>
+
+#if defined(__CUDACC__)
+#define RQ_HD __host__ __device__ __forceinline__
+#else
+#define RQ_HD inline
+#endif
+
+namespace rq {
+
+// ---------------------------------------------------------------- integers
+RQ_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+RQ_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+// Exact IEEE binary64 ops that are never fused (host: -ffp-contract=off TU).
+RQ_HD double dadd(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+RQ_HD double dmul(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+
+// ---------------------------------------------------------------- seeding
+// splitmix64 finaliser with the golden-ratio pre-add (seeding.py:27-32).
+RQ_HD uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+// derive_key(a, b, ...) absorbs parts left to right from h = 0 (seeding.py:35-44).
+RQ_HD uint64_t derive_key2(uint64_t a, uint64_t b) { return splitmix64(splitmix64(a) ^ b); }
+RQ_HD uint64_t derive_key3(uint64_t a, uint64_t b, uint64_t c) {
+  return splitmix64(derive_key2(a, b) ^ c);
+}
+RQ_HD uint64_t derive_key4(uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  return splitmix64(derive_key3(a, b, c) ^ d);
+}
+
+// ---------------------------------------------------------------- numpy PCG64
+// numpy.random.PCG64(SeedSequence(key)): the generator behind derive_rng
+// (seeding.py:59-65).  State/increment as (hi, lo) 64-bit halves.
+struct Pcg64 {
+  uint64_t sh, sl, ih, il;
+  uint32_t spare;
+  int has_spare;
+};
+
+RQ_HD void pcg_step(Pcg64 &g) {
+  const uint64_t MH = 0x2360ED051FC65DA4ULL, ML = 0x4385DF649FCCF645ULL;
+  uint64_t lo = g.sl * ML;
+  uint64_t hi = umulhi64(g.sl, ML) + g.sl * MH + g.sh * ML;
+  uint64_t nl = lo + g.il;
+  hi += g.ih + (nl < lo ? 1u : 0u);
+  g.sl = nl;
+  g.sh = hi;
+}
+
+RQ_HD void pcg_seed(Pcg64 &g, uint64_t key) {
+  // SeedSequence pool mixing (numpy bit_generator.pyx mix_entropy, pool 4).
+  const uint32_t MULT_A = 0x931e8875u, MULT_B = 0x58f38dedu;
+  const uint32_t ML = 0xca01f9ddu, MR = 0x4973f715u;
+  uint32_t ent0 = (uint32_t)key, ent1 = (uint32_t)(key >> 32);
+  int nent = (key >> 32) ? 2 : 1;
+  uint32_t hc = 0x43b0d7e5u;
+  uint32_t pool[4];
+#define RQ_HASHMIX(val, out)  \
+  {                           \
+    uint32_t v_ = (val) ^ hc; \
+    hc *= MULT_A;             \
+    v_ *= hc;                 \
+    out = v_ ^ (v_ >> 16);    \
+  }
+  for (int i = 0; i < 4; i++) {
+    uint32_t e = (i == 0) ? ent0 : ((i == 1 && nent == 2) ? ent1 : 0u);
+    RQ_HASHMIX(e, pool[i]);
+  }
+  for (int s = 0; s < 4; s++)
+    for (int d = 0; d < 4; d++)
+      if (s != d) {
+        uint32_t h;
+        RQ_HASHMIX(pool[s], h);
+        uint32_t r = ML * pool[d] - MR * h;
+        pool[d] = r ^ (r >> 16);
+      }
+#undef RQ_HASHMIX
+  uint32_t w[8];
+  uint32_t hb = 0x8b51f9ddu;
+  for (int i = 0; i < 8; i++) {
+    uint32_t v = pool[i & 3] ^ hb;
+    hb *= MULT_B;
+    v *= hb;
+    w[i] = v ^ (v >> 16);
+  }
+  uint64_t s0 = (uint64_t)w[0] | ((uint64_t)w[1] << 32);  // initstate hi
+  uint64_t s1 = (uint64_t)w[2] | ((uint64_t)w[3] << 32);  // initstate lo
+  uint64_t q0 = (uint64_t)w[4] | ((uint64_t)w[5] << 32);  // initseq hi
+  uint64_t q1 = (uint64_t)w[6] | ((uint64_t)w[7] << 32);  // initseq lo
+  g.ih = (q0 << 1) | (q1 >> 63);
+  g.il = (q1 << 1) | 1u;
+  g.sh = 0;
+  g.sl = 0;
+  pcg_step(g);
+  uint64_t nl = g.sl + s1;
+  g.sh = g.sh + s0 + (nl < s1 ? 1u : 0u);
+  g.sl = nl;
+  pcg_step(g);
+  g.has_spare = 0;
+  g.spare = 0;
+}
+
+RQ_HD uint64_t pcg_next64(Pcg64 &g) {
+  pcg_step(g);
+  uint64_t x = g.sh ^ g.sl;
+  unsigned rot = (unsigned)(g.sh >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+RQ_HD uint32_t pcg_next32(Pcg64 &g) {
+  if (g.has_spare) {
+    g.has_spare = 0;
+    return g.spare;
+  }
+  uint64_t n = pcg_next64(g);
+  g.has_spare = 1;
+  g.spare = (uint32_t)(n >> 32);
+  return (uint32_t)n;
+}
+// Generator.random(): 53 high bits
+RQ_HD double pcg_random(Pcg64 &g) {
+  return (double)(pcg_next64(g) >> 11) * (1.0 / 9007199254740992.0);
+}
+// numpy random_interval(max) for max < 2^32: masked rejection on u32 halves.
+RQ_HD uint32_t pcg_interval32(Pcg64 &g, uint32_t max) {
+  if (max == 0) return 0;
+  uint32_t mask = max;
+  mask |= mask >> 1;
+  mask |= mask >> 2;
+  mask |= mask >> 4;
+  mask |= mask >> 8;
+  mask |= mask >> 16;
+  uint32_t v;
+  do {
+    v = pcg_next32(g) & mask;
+  } while (v > max);
+  return v;
+}
+
+// ---------------------------------------------------------------- Philox-4x32-10
+// Counter (b, path_lo, path_hi, 0), key (k_lo, k_hi) (prng.py:180-212).
+struct U4 {
+  uint32_t x, y, z, w;
+};
+RQ_HD U4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                       uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    uint32_t hi0 = umulhi32(c0, 0xD2511F53u), lo0 = c0 * 0xD2511F53u;
+    uint32_t hi1 = umulhi32(c2, 0xCD9E8D57u), lo1 = c2 * 0xCD9E8D57u;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return U4{c0, c1, c2, c3};
+}
+
+// ---------------------------------------------------------------- SFC64
+// numpy SFC64 core; per-path stream seeded from
+// derive_words(derive_key(seed, 7, m, path), 6) + 12 discarded draws.
+struct Sfc64 {
+  uint64_t a, b, c, w;
+};
+RQ_HD uint64_t sfc_next(Sfc64 &s) {
+  uint64_t tmp = s.a + s.b + s.w++;
+  s.a = s.b ^ (s.b >> 11);
+  s.b = s.c + (s.c << 3);
+  s.c = ((s.c << 24) | (s.c >> 40)) + tmp;
+  return tmp;
+}
+RQ_HD void sfc_seed(Sfc64 &s, uint64_t path_key) {
+  // derive_words(key, 6) = low/high halves of 3 splitmix outputs
+  uint64_t z1 = splitmix64(path_key), z2 = splitmix64(z1), z3 = splitmix64(z2);
+  s.a = z1;
+  s.b = z2;
+  s.c = z3;
+  s.w = 1;
+  for (int i = 0; i < 12; i++) sfc_next(s);
+}
+
+// ---------------------------------------------------------------- division helpers
+// Fast reciprocal: MUFU.RCP64H seed + Newton.  One step leaves ~2^-44
+// relative error, two steps ~1 ulp.
+#if defined(__CUDACC__)
+__device__ __forceinline__ double rcp_seed(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double rcp1(double x) {
+  double r = rcp_seed(x);
+  double e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rcp2(double x) {
+  double r = rcp_seed(x);
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+#endif
+
+// ---------------------------------------------------------------- inverse normal
+// Coefficients of the reference's two-branch rational Phi^-1
+// (models.py:23-64): central in u = (p - 1/2)^2 / R for p >= 0.0465, tail in
+// w = (sqrt(-2 ln p) - V_LO) * V_SCALE; inputs clamped to >= 2^-53.
+struct InvNormal {
+  static constexpr double TINY = 1.1102230246251565e-16;
+  static constexpr double PLOW = 0.0465;
+  static constexpr double RMAX = 0.20566225000000002;
+  static constexpr double VLO = 2.4772173769731336;
+  static constexpr double VSCALE = 0.16408352781008756;
+};
+
+RQ_HD double invn_central_num(double u) {
+  return ((((((-0.2919273214264852 * u + 9.193512285907598) * u + -62.454377324061355) * u +
+            170.0098658859532) * u + -211.46704297849197) * u + 113.93203453144044) * u +
+          -21.62514930947088) * u + 3.8841077977297096;
+}
+RQ_HD double invn_central_den(double u) {
+  return ((((((-0.4290780287479735 * u + 6.969736103714354) * u + -36.143835067804716) * u +
+            83.84882260510376) * u + -93.74669783914054) * u + 47.23127323999088) * u +
+          -8.96090814172393) * u + 1.5495348220676615;
+}
+RQ_HD double invn_tail_num(double w) {
+  return ((((((49.41588603624166 * w + 34.09554370467819) * w + -120.62391569766385) * w +
+            -36.11819081101896) * w + 77.35661807857605) * w + 12.678668433221901) * w +
+          -15.636790505919562) * w + -3.141967925161121;
+}
+RQ_HD double invn_tail_den(double w) {
+  return ((((((-0.0005317355830972598 * w + -8.101041244986659) * w + -2.3666362350675305) * w +
+            19.91298298968798) * w + -1.4094956335739925) * w + -10.941521790794202) * w +
+          1.2762506234112334) * w + 1.8704632131064214;
+}
+
+#if defined(__CUDACC__)
+// Fold p into the lower half: returns pl, sets *neg for p > 1/2.
+__device__ __forceinline__ double invn_fold(double p, bool *neg) {
+  *neg = p > 0.5;
+  double pl = *neg ? 1.0 - p : p;
+  return pl < InvNormal::TINY ? InvNormal::TINY : pl;
+}
+__device__ __forceinline__ double invn_central(double pl) {
+  double q = pl - 0.5;
+  double u = (q * q) * (1.0 / InvNormal::RMAX);
+  return q * invn_central_num(u) * rcp2(invn_central_den(u));
+}
+__device__ __forceinline__ double invn_tail(double pl) {
+  double w = (sqrt(-2.0 * log(pl)) - InvNormal::VLO) * InvNormal::VSCALE;
+  return invn_tail_num(w) * rcp2(invn_tail_den(w));
+}
+// Scalar Phi^-1 (divergent tail); the tile filler uses a compacted tail.
+__device__ __forceinline__ double inv_normal(double p) {
+  bool neg;
+  double pl = invn_fold(p, &neg);
+  double x = pl >= InvNormal::PLOW ? invn_central(pl) : invn_tail(pl);
+  return neg ? -x : x;
+}
+#endif
+
+}  // namespace rq

@@ -1,0 +1,99 @@
+// rq_internal.h -- structures shared by the C-ABI layer (rq_capi.cu) and the
+// kernels (rq_kernels.cu).  Not part of the public ABI (include/rqmc_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace rq {
+
+constexpr int MAX_DIM = 1024;   // Halton/Rasrap dimensions with universal tables
+constexpr int MAX_CAP = 40;     // K + 8 for base 2 (largest digit window)
+constexpr int SOBOL_BITS = 32;  // sobol.py:30
+
+enum Gen : int {
+  GEN_RASRAP_RECURSIVE = 0,
+  GEN_RASRAP_COUNTER = 1,
+  GEN_PHILOX = 2,
+  GEN_SOBOL_GRAY = 3,
+  GEN_SOBOL_COUNTER = 4,
+  GEN_SFC64 = 5,
+};
+enum ModelKind : int { MODEL_LIBOR = 0, MODEL_MBS = 1, MODEL_X1 = 2, MODEL_CONST1 = 3 };
+
+// Per-dimension Halton constants (depend only on the d-th prime).  Offsets
+// are prefix sums over dimensions 0..d-1, identical for every replication.
+struct HaltonDim {
+  int32_t base;     // d-th prime (halton.py:345-350)
+  int32_t K;        // digit_capacity(base) (halton.py:59-66)
+  int32_t cap;      // K + _CAP_PAD (halton.py:38, 262)
+  int32_t ell;      // ceil(log2 base): division by base = (umulhi(t,mlo)+t) >> ell
+  uint32_t mlo;     // low 32 bits of ceil(2^(32+ell)/base)
+  int32_t sig_off;  // offset of sigma_d in a replication's sigma block (sum of bases)
+  int32_t dig_off;  // offset of the start digits (sum of caps)
+  int32_t sum_off;  // offset of partial sums / weight tables (sum of cap+1)
+  double inv_p;     // 1.0 / base
+  double scale0;    // Python pow(inv_p, K): first init-sum weight (halton.py:274)
+};
+
+// Device view of one replication batch's randomisation tables.
+struct RepTables {
+  int gen;
+  int dim;
+  uint64_t seed;
+  int64_t rep_first;   // replication id of local replication 0 (ids start at 1)
+  int32_t rep_count;
+  // Rasrap
+  const double *sigma;     // [rep][sig_stride] permutation values as doubles
+  const uint16_t *digits;  // [rep][dig_stride] base-p digits of the start index n0
+  const double *sums;      // [rep][sum_stride] init partial sums (halton.py:273-278)
+  int64_t sig_stride, dig_stride, sum_stride;
+  // Sobol
+  const uint32_t *sobol_v;     // [rep][dim][32] scrambled direction words
+  const uint32_t *sobol_shift; // [rep][dim]
+};
+
+struct ModelParams {
+  int kind;
+  int dim;
+  double delta, sigma, strike, front_factor;          // LIBOR (models.py:301-322)
+  double i0, k0, k1, k2, k3, k4, sigma_xi, payment;   // MBS (models.py:337-370)
+  const double *table;  // device: LIBOR l0[dim] / MBS ck[dim]
+};
+
+// numpy pairwise-sum plan for one N (see rq_capi.cu build_plan).
+struct SumPlan {
+  int64_t n;
+  int32_t nleaves, nnodes, nlevels;
+  const int64_t *leaf_start;   // [nleaves]
+  const int32_t *leaf_len;     // [nleaves]  (node id of leaf k is k)
+  const int32_t *level_off;    // [nlevels+1] offsets into the internal-node arrays
+  const int32_t *node_id, *node_l, *node_r;  // internal nodes grouped by height
+  int32_t root;
+};
+
+// ---------------------------------------------------------------- launchers
+cudaError_t upload_halton_dims(const HaltonDim *dims, int n, const double *wts,
+                               const double *cscale, int nw);
+cudaError_t launch_rasrap_setup(const RepTables &t, double *sigma, uint16_t *digits,
+                                double *sums, cudaStream_t s);
+cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32_t *gen_v,
+                               uint32_t *shift, cudaStream_t s);
+cudaError_t launch_points(const RepTables &t, int rep_local, int64_t first,
+                          const int64_t *idx, int64_t count, double *out, cudaStream_t s);
+cudaError_t launch_paths(const RepTables &t, const ModelParams &mp, int rep_local0,
+                         int rep_n, int64_t nmax, double *payoffs, int *launched,
+                         cudaStream_t s);
+cudaError_t launch_reduce(const SumPlan &plan, const double *payoffs, int64_t pay_stride,
+                          int reps, double *theta, int theta_stride, double *scratch,
+                          unsigned *tickets, cudaStream_t s);
+cudaError_t launch_model_payoffs(const ModelParams &mp, const double *u, int64_t npaths,
+                                 double *out, cudaStream_t s);
+cudaError_t launch_inv_normal(const double *u, int64_t n, double *out, cudaStream_t s);
+cudaError_t launch_stream_normals(const RepTables &t, int rep_local, int64_t npoints,
+                                  double *block_sums, int nblocks, double *store,
+                                  cudaStream_t s);
+cudaError_t launch_dfma_peak(int blocks, int iters, double *sink, cudaStream_t s);
+constexpr int PEAK_SLOTS_PER_ITER = 16 * 8;  // DFMA per thread per iteration of k_dfma_peak
+int paths_grid_blocks(const RepTables &t, const ModelParams &mp);
+
+}  // namespace rq
