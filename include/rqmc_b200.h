@@ -87,10 +87,11 @@ int rq_sampler_points(rq_sampler *s, int32_t rep_local, int64_t first, int64_t c
 /* sampler.at(indices) (halton.py:507, sobol.py:359, harness.py:69) */
 int rq_sampler_points_at(rq_sampler *s, int32_t rep_local, const int64_t *idx_dev,
                          int64_t count, double *out_dev, void *stream);
-/* Rasrap tables of one replication, for inspection/tests:
- * start_digits_host[sum of (K+8)] (uint16), sigma_host[sum of bases]. */
+/* Rasrap tables of one replication, for inspection/tests (strides padded
+ * to multiples of 4): start digits [sum of (K+8)] uint16, digit
+ * permutations [sum of bases] uint16, init partial sums [sum of (K+9)]. */
 int rq_sampler_rasrap_tables(rq_sampler *s, int32_t rep_local, uint16_t *digits_host,
-                             double *sigma_host, double *sums_host);
+                             uint16_t *sigma_host, double *sums_host);
 
 /* The fused replication engine: for every replication of the sampler and
  * every N in grid (strictly increasing), theta[r][g] = np.sum(payoffs[:N])/N

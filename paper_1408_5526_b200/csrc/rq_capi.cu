@@ -355,7 +355,14 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
     t.sig_stride = T.total_bases(dim);
     t.dig_stride = (T.total_caps(dim) + 3) & ~3;
     t.sum_stride = T.total_sums(dim);
-    size_t b_sig = sizeof(double) * t.sig_stride * rep_count;
+    t.sig_stride = (t.sig_stride + 3) & ~3;
+    t.sig_chunk_max = 0;
+    for (int d0 = 0; d0 < dim; d0 += rq::CHUNK_DIMS) {
+      int d1 = std::min(dim, d0 + rq::CHUNK_DIMS) - 1;
+      t.sig_chunk_max = std::max(t.sig_chunk_max,
+                                 T.dims[d1].sig_off + T.dims[d1].base - T.dims[d0].sig_off);
+    }
+    size_t b_sig = sizeof(uint16_t) * t.sig_stride * rep_count;
     size_t b_sum = sizeof(double) * t.sum_stride * rep_count;
     size_t b_dig = sizeof(uint16_t) * t.dig_stride * rep_count;
     cudaError_t e = cudaMallocAsync(&S->mem, b_sig + b_sum + b_dig, s);
@@ -364,9 +371,9 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
       return fail(RQ_ERR_CUDA, "allocating rasrap tables (%zu B): %s", b_sig + b_sum + b_dig,
                   cudaGetErrorString(e));
     }
-    double *sig = (double *)S->mem;
-    double *sums = sig + t.sig_stride * rep_count;
-    uint16_t *dig = (uint16_t *)(sums + t.sum_stride * rep_count);
+    double *sums = (double *)S->mem;
+    uint16_t *sig = (uint16_t *)(sums + t.sum_stride * rep_count);
+    uint16_t *dig = sig + t.sig_stride * rep_count;
     t.sigma = sig;
     t.sums = sums;
     t.digits = dig;
@@ -449,7 +456,7 @@ int rq_sampler_points_at(rq_sampler *s, int32_t rep_local, const int64_t *idx_de
 }
 
 int rq_sampler_rasrap_tables(rq_sampler *s, int32_t rep_local, uint16_t *digits_host,
-                             double *sigma_host, double *sums_host) {
+                             uint16_t *sigma_host, double *sums_host) {
   int rc = check_rep(s, rep_local);
   if (rc) return rc;
   const rq::RepTables &t = s->t;
@@ -461,7 +468,7 @@ int rq_sampler_rasrap_tables(rq_sampler *s, int32_t rep_local, uint16_t *digits_
                        sizeof(uint16_t) * t.dig_stride, cudaMemcpyDeviceToHost));
   if (sigma_host)
     RQ_CUDA(cudaMemcpy(sigma_host, t.sigma + rep_local * t.sig_stride,
-                       sizeof(double) * t.sig_stride, cudaMemcpyDeviceToHost));
+                       sizeof(uint16_t) * t.sig_stride, cudaMemcpyDeviceToHost));
   if (sums_host)
     RQ_CUDA(cudaMemcpy(sums_host, t.sums + rep_local * t.sum_stride,
                        sizeof(double) * t.sum_stride, cudaMemcpyDeviceToHost));

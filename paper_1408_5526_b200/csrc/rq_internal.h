@@ -9,6 +9,7 @@ namespace rq {
 constexpr int MAX_DIM = 1024;   // Halton/Rasrap dimensions with universal tables
 constexpr int MAX_CAP = 40;     // K + 8 for base 2 (largest digit window)
 constexpr int SOBOL_BITS = 32;  // sobol.py:30
+constexpr int CHUNK_DIMS = 20;  // dimensions per generator chunk in the fused kernels
 
 enum Gen : int {
   GEN_RASRAP_RECURSIVE = 0,
@@ -43,10 +44,11 @@ struct RepTables {
   int64_t rep_first;   // replication id of local replication 0 (ids start at 1)
   int32_t rep_count;
   // Rasrap
-  const double *sigma;     // [rep][sig_stride] permutation values as doubles
+  const uint16_t *sigma;   // [rep][sig_stride] digit permutations sigma_d
   const uint16_t *digits;  // [rep][dig_stride] base-p digits of the start index n0
   const double *sums;      // [rep][sum_stride] init partial sums (halton.py:273-278)
   int64_t sig_stride, dig_stride, sum_stride;
+  int32_t sig_chunk_max;   // max over CHUNK-dim groups of the sigma entries they need
   // Sobol
   const uint32_t *sobol_v;     // [rep][dim][32] scrambled direction words
   const uint32_t *sobol_shift; // [rep][dim]
@@ -74,7 +76,7 @@ struct SumPlan {
 // ---------------------------------------------------------------- launchers
 cudaError_t upload_halton_dims(const HaltonDim *dims, int n, const double *wts,
                                const double *cscale, int nw);
-cudaError_t launch_rasrap_setup(const RepTables &t, double *sigma, uint16_t *digits,
+cudaError_t launch_rasrap_setup(const RepTables &t, uint16_t *sigma, uint16_t *digits,
                                 double *sums, cudaStream_t s);
 cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32_t *gen_v,
                                uint32_t *shift, cudaStream_t s);

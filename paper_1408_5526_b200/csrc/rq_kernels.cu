@@ -28,7 +28,7 @@
 namespace rq {
 
 constexpr int TILE = 128;  // paths per CTA tile = threads per CTA
-constexpr int CHUNK = 20;  // dimensions per generator chunk (multiple of 4 for Philox)
+constexpr int CHUNK = CHUNK_DIMS;  // dimensions per generator chunk (multiple of 4 for Philox)
 constexpr int WARPS = TILE / 32;
 
 __constant__ HaltonDim c_hdim[MAX_DIM];
@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t div_base(uint32_t t, const HaltonDim &h) {
 
 // One thread per (replication, dimension): rasrap_config + RasrapStream
 // init (halton.py:345-360, 256-278, 139-155; seeding.py:59-65).
-__global__ void k_rasrap_setup(RepTables t, double *sigma, uint16_t *digits, double *sums) {
+__global__ void k_rasrap_setup(RepTables t, uint16_t *sigma, uint16_t *digits, double *sums) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)t.rep_count * t.dim) return;
   int rl = (int)(gid / t.dim), d = (int)(gid % t.dim);
@@ -68,11 +68,11 @@ __global__ void k_rasrap_setup(RepTables t, double *sigma, uint16_t *digits, dou
   Pcg64 g;
   pcg_seed(g, derive_key2(key, (uint64_t)d));  // derive_rng(seed, i)
   uint64_t k53 = pcg_next64(g) >> 11;          // rng.random() = k53 * 2^-53
-  double *sg = sigma + (int64_t)rl * t.sig_stride + h.sig_off;
-  for (int a = 0; a < h.base; a++) sg[a] = (double)a;
+  uint16_t *sg = sigma + (int64_t)rl * t.sig_stride + h.sig_off;
+  for (int a = 0; a < h.base; a++) sg[a] = (uint16_t)a;
   for (int i = h.base - 1; i >= 1; i--) {  // rng.permutation(p)
     int j = (int)pcg_interval32(g, (uint32_t)i);
-    double tmp = sg[j];
+    uint16_t tmp = sg[j];
     sg[j] = sg[i];
     sg[i] = tmp;
   }
@@ -92,7 +92,7 @@ __global__ void k_rasrap_setup(RepTables t, double *sigma, uint16_t *digits, dou
   for (int j = h.K; j <= h.cap; j++) sm[j] = 0.0;
   double scale = h.scale0;
   for (int j = h.K - 1; j >= 0; j--) {
-    sm[j] = dadd(sm[j + 1], dmul(sg[dg[j]], scale));
+    sm[j] = dadd(sm[j + 1], dmul((double)sg[dg[j]], scale));
     scale = dmul(scale, (double)h.base);
   }
 }
@@ -124,53 +124,187 @@ __global__ void k_sobol_setup(RepTables t, const uint32_t *v, uint32_t *gen_v,
 }
 
 // ======================================================================
-// Generators: thread-per-path, uniforms for dims [d0, d0+Dc) into a
-// shared-memory column (stride TILE).
+// Generators.  Every thread produces the uniforms of ITS point for dims
+// [d0, d0+Dc) into a shared-memory column (stride TILE).  Interface:
+//   begin(t, rl, base, path, sh, sig_dyn, sig_cap)  per thread
+//   prepare(d0, Dc)   block-cooperative (all threads, may __syncthreads)
+//   chunk(d0, Dc, zcol)
+// "Tiled" generators assume path = base + threadIdx.x (consecutive points);
+// "direct" ones take any path index (sampler.at).
 // ======================================================================
+constexpr int LW = 16;            // low digit window handled per thread (tiled Rasrap)
+constexpr int SIG_SMEM_MAX = 16384;  // u16 sigma entries staged per chunk
 
-// Rasrap recursive form (Alg. 2, halton.py:392-416), evaluated at any index
-// without replaying the stream: for n = n0 + i let h be the highest digit
-// where n and n0 differ (= highest carry the odometer reached).  The stream
-// holds sums[j] = init_sums[j] above h and the chain
-// S_j = S_{j+1} + sigma(a_j) * binpow(1/p, j+1) below, so the point is that
-// chain started from init_sums[h+1] -- bit-identical to the reference.
-struct GenRasrapRec {
-  const double *sig, *sums;
-  const uint16_t *dig;
-  uint32_t i;
-  uint16_t *scr;  // this thread's digit scratch column [MAX_CAP][TILE]
+struct RasrapTileShared {
+  double pb[CHUNK][LW + 1];      // stream partial sums at the tile base B, positions 0..LW
+  double wt[CHUNK][LW];          // binpow weights of positions 0..LW-1
+  uint16_t bd[CHUNK][LW];        // base-p digits of B, positions 0..LW-1
+  uint16_t bfull[CHUNK][MAX_CAP];
+  int32_t soff[CHUNK];           // sigma offset of the dim (staged or global)
+  int32_t lim[CHUNK];            // min(LW, cap)
+  uint16_t scr[LW][TILE];        // per-thread digits of n = B + t
+};
+struct SobolTileShared {
+  uint32_t lowtab[CHUNK][128];   // XOR of v_k over the set bits k < 7
+  uint32_t xhi[CHUNK];           // shift ^ XOR of v_k over the tile's bits k >= 7
+};
+union GenShared {
+  RasrapTileShared r;
+  SobolTileShared s;
+};
 
-  __device__ void begin(const RepTables &t, int rl, uint64_t path, uint16_t *scratch) {
-    sig = t.sigma + (int64_t)rl * t.sig_stride;
-    sums = t.sums + (int64_t)rl * t.sum_stride;
-    dig = t.digits + (int64_t)rl * t.dig_stride;
-    i = (uint32_t)path;
-    scr = scratch;
+__device__ __forceinline__ double u16d(uint16_t v) { return (double)v; }
+
+// Recursive-form point at arbitrary index (Alg. 2, halton.py:392-416)
+// evaluated without replaying the stream: for n = n0 + i let h be the
+// highest digit where n and n0 differ (= highest carry the odometer
+// reached).  The stream then holds sums[j] = init_sums[j] above h and the
+// chain S_j = S_{j+1} + sigma(a_j) * binpow(1/p, j+1) below, so the point is
+// that chain started from init_sums[h+1] -- bit-identical to the reference.
+__device__ double rasrap_rec_direct(const RepTables &t, int rl, int d, uint32_t i,
+                                    uint16_t *scr) {
+  const HaltonDim &h = c_hdim[d];
+  const uint16_t *d0 = t.digits + (int64_t)rl * t.dig_stride + h.dig_off;
+  const uint16_t *sg = t.sigma + (int64_t)rl * t.sig_stride + h.sig_off;
+  const double *sums = t.sums + (int64_t)rl * t.sum_stride + h.sum_off;
+  uint32_t r = i, carry = 0;
+  int hi = -1, j = 0;
+  while (r != 0u || carry != 0u) {
+    uint32_t q = div_base(r, h);
+    uint32_t a0 = d0[j];
+    uint32_t a = a0 + (r - q * (uint32_t)h.base) + carry;
+    carry = a >= (uint32_t)h.base;
+    a = carry ? a - (uint32_t)h.base : a;
+    scr[j * TILE] = (uint16_t)a;
+    hi = (a != a0) ? j : hi;
+    r = q;
+    j++;
   }
-  __device__ __forceinline__ double value(int d) const {
-    const HaltonDim &h = c_hdim[d];
-    const uint16_t *d0 = dig + h.dig_off;
-    uint32_t t = i, carry = 0;
-    int hi = -1, j = 0;
-    while (t != 0u || carry != 0u) {
-      uint32_t q = div_base(t, h);
-      uint32_t a0 = d0[j];
-      uint32_t a = a0 + (t - q * (uint32_t)h.base) + carry;
-      carry = a >= (uint32_t)h.base;
-      a = carry ? a - (uint32_t)h.base : a;
+  const double *w = g_wts + h.sum_off;
+  double S = sums[hi + 1];
+  for (int k = hi; k >= 0; k--) S = dadd(S, dmul(u16d(sg[scr[k * TILE]]), w[k]));
+  return S;
+}
+
+struct GenRasrapRecDirect {
+  const RepTables *t;
+  int rl;
+  uint32_t i;
+  uint16_t *scr;
+  __device__ void begin(const RepTables &t_, int rl_, uint64_t, uint64_t path, GenShared &sh,
+                        uint16_t *, int) {
+    t = &t_;
+    rl = rl_;
+    i = (uint32_t)path;
+    scr = &sh.r.scr[0][0] + threadIdx.x;
+  }
+  __device__ void prepare(int, int) {}
+  __device__ void chunk(int d0, int Dc, double *zcol) {
+    for (int dd = 0; dd < Dc; dd++) zcol[dd * TILE] = rasrap_rec_direct(*t, rl, d0 + dd, i, scr);
+  }
+};
+
+// Tiled recursive form.  prepare() builds, per dim of the chunk, the stream
+// state at the tile base B = n0 + base (digits + partial sums P_B[0..LW]);
+// a thread then adds its offset t < TILE to B's low digits and re-chains
+// from P_B[h_t + 1], h_t = highest digit changed by the addition.  This is
+// the same value (above h_t the stream at n equals the stream at B), with
+// ~log_p(TILE) digit positions per point instead of ~log_p(n), and every
+// table access in shared memory.  Carries that run past the window fall
+// back to the direct evaluation.
+struct GenRasrapRecTile {
+  const RepTables *t;
+  int rl;
+  uint32_t base;
+  GenShared *sh;
+  const uint16_t *sig;  // staged (smem) or global sigma of the replication
+  uint16_t *sig_dyn;
+  int sig_cap;
+  __device__ void begin(const RepTables &t_, int rl_, uint64_t base_, uint64_t, GenShared &s,
+                        uint16_t *sig_dyn_, int sig_cap_) {
+    t = &t_;
+    rl = rl_;
+    base = (uint32_t)base_;
+    sh = &s;
+    sig_dyn = sig_dyn_;
+    sig_cap = sig_cap_;
+  }
+  __device__ void prepare(int d0, int Dc) {
+    RasrapTileShared &R = sh->r;
+    const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
+    const int off0 = c_hdim[d0].sig_off;
+    const int nsig = c_hdim[d0 + Dc - 1].sig_off + c_hdim[d0 + Dc - 1].base - off0;
+    const bool staged = nsig <= sig_cap;
+    __syncthreads();  // previous chunk is done with the shared state
+    if (staged) {
+      for (int k = threadIdx.x; k < nsig; k += TILE) sig_dyn[k] = gsig[off0 + k];
+      sig = sig_dyn;
+    } else {
+      sig = gsig;
+    }
+    if (threadIdx.x < Dc) {
+      const int dd = threadIdx.x;
+      const HaltonDim h = c_hdim[d0 + dd];
+      const uint32_t p = (uint32_t)h.base;
+      const uint16_t *n0 = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
+      const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
+      const uint16_t *sg = gsig + h.sig_off;
+      const double *w = g_wts + h.sum_off;
+      // digits of B = n0 + base
+      uint32_t r = base, carry = 0;
+      int hB = -1;
+      for (int j = 0; j < h.cap; j++) {
+        uint32_t q = div_base(r, h);
+        uint32_t a0 = n0[j];
+        uint32_t a = a0 + (r - q * p) + carry;
+        carry = a >= p;
+        a = carry ? a - p : a;
+        R.bfull[dd][j] = (uint16_t)a;
+        hB = (a != a0) ? j : hB;
+        r = q;
+      }
+      const int lim = LW < h.cap ? LW : h.cap;
+      R.lim[dd] = lim;
+      for (int j = lim; j > hB; j--) R.pb[dd][j] = ini[j];
+      double S = ini[hB + 1];
+      for (int j = hB; j >= 0; j--) {
+        S = dadd(S, dmul(u16d(sg[R.bfull[dd][j]]), w[j]));
+        if (j <= lim) R.pb[dd][j] = S;
+      }
+      for (int j = 0; j < lim; j++) {
+        R.bd[dd][j] = R.bfull[dd][j];
+        R.wt[dd][j] = w[j];
+      }
+      R.soff[dd] = staged ? h.sig_off - off0 : h.sig_off;
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ double value(int d, int dd) const {
+    const RasrapTileShared &R = sh->r;
+    const uint32_t p = (uint32_t)c_hdim[d].base;
+    const int lim = R.lim[dd];
+    uint16_t *scr = const_cast<uint16_t *>(&R.scr[0][0]) + threadIdx.x;
+    uint32_t r = threadIdx.x, carry = 0;
+    int h = -1, j = 0;
+    while (r != 0u || carry != 0u) {
+      if (j >= lim) return rasrap_rec_direct(*t, rl, d, base + threadIdx.x, scr);
+      uint32_t q = div_base(r, c_hdim[d]);
+      uint32_t b = R.bd[dd][j];
+      uint32_t a = b + (r - q * p) + carry;
+      carry = a >= p;
+      a = carry ? a - p : a;
       scr[j * TILE] = (uint16_t)a;
-      hi = (a != a0) ? j : hi;
-      t = q;
+      h = (a != b) ? j : h;
+      r = q;
       j++;
     }
-    const double *sg = sig + h.sig_off;
-    const double *w = g_wts + h.sum_off;
-    double S = sums[h.sum_off + hi + 1];
-    for (int k = hi; k >= 0; k--) S = dadd(S, dmul(__ldg(sg + scr[k * TILE]), w[k]));
+    const uint16_t *sg = sig + R.soff[dd];
+    double S = R.pb[dd][h + 1];
+    for (int k = h; k >= 0; k--) S = dadd(S, dmul(u16d(sg[scr[k * TILE]]), R.wt[dd][k]));
     return S;
   }
   __device__ void chunk(int d0, int Dc, double *zcol) {
-    for (int dd = 0; dd < Dc; dd++) zcol[dd * TILE] = value(d0 + dd);
+    for (int dd = 0; dd < Dc; dd++) zcol[dd * TILE] = value(d0 + dd, dd);
   }
 };
 
@@ -178,18 +312,19 @@ struct GenRasrapRec {
 // from the least significant digit up, scale_j = (1/p)^(j+1) by repeated
 // multiplication, over max(K, #digits) positions.
 struct GenRasrapCounter {
-  const double *sig;
-  const uint16_t *dig;
+  const uint16_t *sig, *dig;
   uint32_t i;
-  __device__ void begin(const RepTables &t, int rl, uint64_t path, uint16_t *) {
+  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
+                        uint16_t *, int) {
     sig = t.sigma + (int64_t)rl * t.sig_stride;
     dig = t.digits + (int64_t)rl * t.dig_stride;
     i = (uint32_t)path;
   }
+  __device__ void prepare(int, int) {}
   __device__ __forceinline__ double value(int d) const {
     const HaltonDim &h = c_hdim[d];
     const uint16_t *d0 = dig + h.dig_off;
-    const double *sg = sig + h.sig_off;
+    const uint16_t *sg = sig + h.sig_off;
     const double *cs = g_cscale + h.sum_off;
     uint32_t t = i, carry = 0;
     double x = 0.0;
@@ -198,7 +333,7 @@ struct GenRasrapCounter {
       uint32_t a = d0[j] + (t - q * (uint32_t)h.base) + carry;
       carry = a >= (uint32_t)h.base;
       a = carry ? a - (uint32_t)h.base : a;
-      x = dadd(x, dmul(__ldg(sg + a), cs[j]));
+      x = dadd(x, dmul(u16d(sg[a]), cs[j]));
       t = q;
     }
     return x;
@@ -212,13 +347,15 @@ struct GenRasrapCounter {
 // (prng.py:180-231, harness.py:53-67).
 struct GenPhilox {
   uint32_t k0, k1, plo, phi;
-  __device__ void begin(const RepTables &t, int rl, uint64_t path, uint16_t *) {
+  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
+                        uint16_t *, int) {
     uint64_t key = derive_key3(t.seed, 3, (uint64_t)(t.rep_first + rl));
     k0 = (uint32_t)key;
     k1 = (uint32_t)(key >> 32);
     plo = (uint32_t)path;
     phi = (uint32_t)(path >> 32);
   }
+  __device__ void prepare(int, int) {}
   __device__ void chunk(int d0, int Dc, double *zcol) {  // d0 % 4 == 0
     for (int dd = 0; dd < Dc; dd += 4) {
       U4 w = philox4x32_10((uint32_t)((d0 + dd) >> 2), plo, phi, 0u, k0, k1);
@@ -235,14 +372,16 @@ struct GenPhilox {
 // pre-scrambled direction words over the set bits of j, XOR the shift;
 // the Gray-code sampler's point i is the counter point at i ^ (i >> 1).
 template <bool GRAY>
-struct GenSobol {
+struct GenSobolDirect {
   const uint32_t *v, *shift;
   uint64_t idx;
-  __device__ void begin(const RepTables &t, int rl, uint64_t path, uint16_t *) {
+  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
+                        uint16_t *, int) {
     v = t.sobol_v + (int64_t)rl * t.dim * SOBOL_BITS;
     shift = t.sobol_shift + (int64_t)rl * t.dim;
     idx = GRAY ? (path ^ (path >> 1)) : path;
   }
+  __device__ void prepare(int, int) {}
   __device__ void chunk(int d0, int Dc, double *zcol) {
     for (int dd = 0; dd < Dc; dd++) {
       const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
@@ -258,15 +397,77 @@ struct GenSobol {
   }
 };
 
+// Tiled Sobol': the index bits >= 7 are shared by a 128-aligned tile, so
+// prepare() folds them (and the shift) into one word per dim and tabulates
+// the 128 low-bit XOR patterns; a point is then one table lookup.  Tiles
+// that are not 128-aligned (sampler.fill from an odd start) take the
+// direct loop.
+template <bool GRAY>
+struct GenSobolTile {
+  const uint32_t *v, *shift;
+  uint32_t idx, hi_key;
+  bool aligned;
+  GenShared *sh;
+  __device__ void begin(const RepTables &t, int rl, uint64_t base, uint64_t path, GenShared &s,
+                        uint16_t *, int) {
+    v = t.sobol_v + (int64_t)rl * t.dim * SOBOL_BITS;
+    shift = t.sobol_shift + (int64_t)rl * t.dim;
+    uint32_t i = (uint32_t)path, b = (uint32_t)base;
+    idx = GRAY ? (i ^ (i >> 1)) : i;
+    uint32_t bidx = GRAY ? (b ^ (b >> 1)) : b;
+    hi_key = bidx >> 7;
+    aligned = (b & 127u) == 0u;
+    sh = &s;
+  }
+  __device__ void prepare(int d0, int Dc) {
+    SobolTileShared &S = sh->s;
+    __syncthreads();
+    if (aligned) {
+      for (int e = threadIdx.x; e < Dc * 128; e += TILE) {
+        int dd = e >> 7, x = e & 127;
+        const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
+        uint32_t acc = 0;
+        for (int k = 0; k < 7; k++)
+          if (x & (1 << k)) acc ^= vd[k];
+        S.lowtab[dd][x] = acc;
+      }
+      if (threadIdx.x < Dc) {
+        const uint32_t *vd = v + (d0 + threadIdx.x) * SOBOL_BITS;
+        uint32_t acc = shift[d0 + threadIdx.x], bits = hi_key;
+        for (int k = 7; bits; k++, bits >>= 1)
+          if (bits & 1u) acc ^= vd[k];
+        S.xhi[threadIdx.x] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  __device__ void chunk(int d0, int Dc, double *zcol) {
+    const SobolTileShared &S = sh->s;
+    for (int dd = 0; dd < Dc; dd++) {
+      uint32_t x;
+      if (aligned) {
+        x = S.xhi[dd] ^ S.lowtab[dd][idx & 127u];
+      } else {
+        const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
+        x = shift[d0 + dd];
+        for (uint32_t bits = idx; bits; bits &= bits - 1u) x ^= vd[__ffs(bits) - 1];
+      }
+      zcol[dd * TILE] = (double)x * 2.3283064365386963e-10;
+    }
+  }
+};
+
 // SFC64 per-path stream (no reference counterpart; numpy SFC64 core):
 // state from derive_words(derive_key(seed, 7, m, path), 6), 12 warm-up
 // draws, u = (w >> 11) 2^-53 as numpy Generator.random().
 struct GenSfc64 {
   Sfc64 s;
-  __device__ void begin(const RepTables &t, int rl, uint64_t path, uint16_t *) {
+  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
+                        uint16_t *, int) {
     uint64_t km = derive_key3(t.seed, 7, (uint64_t)(t.rep_first + rl));
     sfc_seed(s, splitmix64(km ^ path));
   }
+  __device__ void prepare(int, int) {}
   __device__ void chunk(int d0, int Dc, double *zcol) {
     for (int dd = 0; dd < Dc; dd++)
       zcol[dd * TILE] = (double)(sfc_next(s) >> 11) * (1.0 / 9007199254740992.0);
@@ -398,33 +599,38 @@ struct PathArgs {
   int64_t nmax;
   int64_t tiles_per_rep;
   double *payoffs;  // [rep_n][nmax]
+  int sig_cap;      // u16 sigma entries staged per chunk (0: read from global)
 };
 
-template <class G>
-__device__ __forceinline__ void gen_chunk(G &g, int d0, int Dc, double *zcol) {
-  g.chunk(d0, Dc, zcol);
+// dynamic shared memory: [model table doubles][staged sigma u16]
+__device__ __forceinline__ uint16_t *dyn_sig(void *dyn, int table_doubles) {
+  return reinterpret_cast<uint16_t *>(reinterpret_cast<double *>(dyn) + table_doubles);
 }
 
 template <class G, int S>
 __global__ void __launch_bounds__(TILE) k_paths_libor(PathArgs a) {
   __shared__ double zt[CHUNK * TILE];
   __shared__ uint16_t tq[WARPS][CHUNK * 32];
-  __shared__ uint16_t scr[MAX_CAP * TILE];
+  __shared__ GenShared gsh;
   __shared__ double l0s[S];
+  extern __shared__ double dyn[];
+  uint16_t *sig_dyn = dyn_sig(dyn, 0);
   for (int n = threadIdx.x; n < S; n += TILE) l0s[n] = a.mp.table[n];
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
   for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
     const int rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
-    const int64_t path = (w % a.tiles_per_rep) * TILE + threadIdx.x;
+    const int64_t base = (w % a.tiles_per_rep) * TILE;
+    const int64_t path = base + threadIdx.x;
     G g;
-    g.begin(a.t, rl, (uint64_t)path, scr + threadIdx.x);
+    g.begin(a.t, rl, (uint64_t)base, (uint64_t)path, gsh, sig_dyn, a.sig_cap);
     ModelLibor<S> md;
     md.begin(a.mp, l0s);
     for (int d0 = 0; d0 < S; d0 += CHUNK) {
       const int Dc = S - d0 < CHUNK ? S - d0 : CHUNK;
-      gen_chunk(g, d0, Dc, zt + threadIdx.x);
+      g.prepare(d0, Dc);
+      g.chunk(d0, Dc, zt + threadIdx.x);
       __syncwarp();
       chunk_to_normals(zt, Dc, tq[warp]);
       md.chunk(d0, Dc, zt + threadIdx.x, TILE);
@@ -439,22 +645,26 @@ template <class G>
 __global__ void __launch_bounds__(TILE) k_paths_mbs(PathArgs a) {
   __shared__ double zt[CHUNK * TILE];
   __shared__ uint16_t tq[WARPS][CHUNK * 32];
-  __shared__ uint16_t scr[MAX_CAP * TILE];
-  extern __shared__ double cks[];
+  __shared__ GenShared gsh;
+  extern __shared__ double dyn[];
+  double *cks = dyn;
+  uint16_t *sig_dyn = dyn_sig(dyn, a.mp.dim);
   for (int n = threadIdx.x; n < a.mp.dim; n += TILE) cks[n] = a.mp.table[n];
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
   for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
     const int rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
-    const int64_t path = (w % a.tiles_per_rep) * TILE + threadIdx.x;
+    const int64_t base = (w % a.tiles_per_rep) * TILE;
+    const int64_t path = base + threadIdx.x;
     G g;
-    g.begin(a.t, rl, (uint64_t)path, scr + threadIdx.x);
+    g.begin(a.t, rl, (uint64_t)base, (uint64_t)path, gsh, sig_dyn, a.sig_cap);
     ModelMbs md;
     md.begin(a.mp, cks);
     for (int d0 = 0; d0 < a.mp.dim; d0 += CHUNK) {
       const int Dc = a.mp.dim - d0 < CHUNK ? a.mp.dim - d0 : CHUNK;
-      gen_chunk(g, d0, Dc, zt + threadIdx.x);
+      g.prepare(d0, Dc);
+      g.chunk(d0, Dc, zt + threadIdx.x);
       __syncwarp();
       chunk_to_normals(zt, Dc, tq[warp]);
       md.chunk(d0, Dc, zt + threadIdx.x, TILE, a.mp);
@@ -468,16 +678,20 @@ __global__ void __launch_bounds__(TILE) k_paths_mbs(PathArgs a) {
 template <class G, bool CONST1>
 __global__ void __launch_bounds__(TILE) k_paths_test(PathArgs a) {
   __shared__ double zt[TILE];
-  __shared__ uint16_t scr[MAX_CAP * TILE];
+  __shared__ GenShared gsh;
+  extern __shared__ double dyn[];
+  uint16_t *sig_dyn = dyn_sig(dyn, 0);
   const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
   for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
     const int rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
-    const int64_t path = (w % a.tiles_per_rep) * TILE + threadIdx.x;
+    const int64_t base = (w % a.tiles_per_rep) * TILE;
+    const int64_t path = base + threadIdx.x;
     double f = 1.0;
     if (!CONST1) {
       G g;
-      g.begin(a.t, rl, (uint64_t)path, scr + threadIdx.x);
-      gen_chunk(g, 0, 1, zt + threadIdx.x);
+      g.begin(a.t, rl, (uint64_t)base, (uint64_t)path, gsh, sig_dyn, a.sig_cap);
+      g.prepare(0, 1);
+      g.chunk(0, 1, zt + threadIdx.x);
       f = zt[threadIdx.x];
     }
     if (path < a.nmax) a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = f;
@@ -485,23 +699,27 @@ __global__ void __launch_bounds__(TILE) k_paths_test(PathArgs a) {
 }
 
 // ======================================================================
-// Point kernels (sampler.fill / sampler.at), out[count][dim] row-major
+// Point kernels (sampler.fill / sampler.at), out[count][dim] row-major.
+// Consecutive rows use the tiled generators, explicit indices the direct.
 // ======================================================================
 template <class G>
 __global__ void __launch_bounds__(TILE) k_points(RepTables t, int rl, int64_t first,
                                                  const int64_t *idx, int64_t count,
-                                                 double *out) {
+                                                 double *out, int sig_cap) {
   __shared__ double zt[CHUNK * TILE];
-  __shared__ uint16_t scr[MAX_CAP * TILE];
-  for (int64_t base = (int64_t)blockIdx.x * TILE; base < count; base += (int64_t)gridDim.x * TILE) {
-    const int64_t r = base + threadIdx.x;
+  __shared__ GenShared gsh;
+  extern __shared__ double dyn[];
+  uint16_t *sig_dyn = dyn_sig(dyn, 0);
+  for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < count; tb += (int64_t)gridDim.x * TILE) {
+    const int64_t r = tb + threadIdx.x;
     const bool ok = r < count;
-    const int64_t path = ok ? (idx ? idx[r] : first + r) : first;
+    const int64_t path = idx ? (ok ? idx[r] : 0) : first + r;
     G g;
-    g.begin(t, rl, (uint64_t)path, scr + threadIdx.x);
+    g.begin(t, rl, (uint64_t)(first + tb), (uint64_t)path, gsh, sig_dyn, sig_cap);
     for (int d0 = 0; d0 < t.dim; d0 += CHUNK) {
       const int Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
-      gen_chunk(g, d0, Dc, zt + threadIdx.x);
+      g.prepare(d0, Dc);
+      g.chunk(d0, Dc, zt + threadIdx.x);
       if (ok)
         for (int dd = 0; dd < Dc; dd++) out[r * t.dim + d0 + dd] = zt[dd * TILE + threadIdx.x];
     }
@@ -603,22 +821,24 @@ __global__ void k_reduce(SumPlan plan, const double *pay, int64_t pay_stride, do
 // ======================================================================
 template <class G>
 __global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t npoints,
-                                                 double *block_sums, double *store) {
+                                                 double *block_sums, double *store, int sig_cap) {
   __shared__ double zt[CHUNK * TILE];
   __shared__ uint16_t tq[WARPS][CHUNK * 32];
-  __shared__ uint16_t scr[MAX_CAP * TILE];
+  __shared__ GenShared gsh;
   __shared__ double red[WARPS];
+  extern __shared__ double dyn[];
+  uint16_t *sig_dyn = dyn_sig(dyn, 0);
   const int warp = threadIdx.x >> 5;
   double acc = 0.0;
-  for (int64_t base = (int64_t)blockIdx.x * TILE; base < npoints;
-       base += (int64_t)gridDim.x * TILE) {
-    const int64_t r = base + threadIdx.x;
+  for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < npoints; tb += (int64_t)gridDim.x * TILE) {
+    const int64_t r = tb + threadIdx.x;
     const bool ok = r < npoints;
     G g;
-    g.begin(t, rl, (uint64_t)(ok ? r : 0), scr + threadIdx.x);
+    g.begin(t, rl, (uint64_t)tb, (uint64_t)r, gsh, sig_dyn, sig_cap);
     for (int d0 = 0; d0 < t.dim; d0 += CHUNK) {
       const int Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
-      gen_chunk(g, d0, Dc, zt + threadIdx.x);
+      g.prepare(d0, Dc);
+      g.chunk(d0, Dc, zt + threadIdx.x);
       __syncwarp();
       chunk_to_normals(zt, Dc, tq[warp]);
       if (ok) {
@@ -690,7 +910,7 @@ static int persistent_blocks(K kernel, size_t dyn_smem, int64_t work) {
   return (int)(work < b ? (work < 1 ? 1 : work) : b);
 }
 
-cudaError_t launch_rasrap_setup(const RepTables &t, double *sigma, uint16_t *digits,
+cudaError_t launch_rasrap_setup(const RepTables &t, uint16_t *sigma, uint16_t *digits,
                                 double *sums, cudaStream_t s) {
   int64_t n = (int64_t)t.rep_count * t.dim;
   int blocks = (int)((n + 127) / 128);
@@ -706,23 +926,39 @@ cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32
   return cudaGetLastError();
 }
 
+static int sig_cap_for(const RepTables &t) {
+  return (t.gen == GEN_RASRAP_RECURSIVE && t.sig_chunk_max <= SIG_SMEM_MAX) ? t.sig_chunk_max : 0;
+}
+static size_t dyn_bytes(int table_doubles, int sig_cap) {
+  return sizeof(double) * table_doubles + sizeof(uint16_t) * sig_cap;
+}
+
 template <class G>
 static cudaError_t points_t(const RepTables &t, int rl, int64_t first, const int64_t *idx,
                             int64_t count, double *out, cudaStream_t s) {
   int64_t tiles = (count + TILE - 1) / TILE;
-  int blocks = persistent_blocks(k_points<G>, 0, tiles);
-  k_points<G><<<blocks, TILE, 0, s>>>(t, rl, first, idx, count, out);
+  int cap = idx ? 0 : sig_cap_for(t);
+  size_t dyn = dyn_bytes(0, cap);
+  int blocks = persistent_blocks(k_points<G>, dyn, tiles);
+  k_points<G><<<blocks, TILE, dyn, s>>>(t, rl, first, idx, count, out, cap);
   return cudaGetLastError();
 }
 
 cudaError_t launch_points(const RepTables &t, int rl, int64_t first, const int64_t *idx,
                           int64_t count, double *out, cudaStream_t s) {
+  const bool at = idx != nullptr;
   switch (t.gen) {
-    case GEN_RASRAP_RECURSIVE: return points_t<GenRasrapRec>(t, rl, first, idx, count, out, s);
+    case GEN_RASRAP_RECURSIVE:
+      return at ? points_t<GenRasrapRecDirect>(t, rl, first, idx, count, out, s)
+                : points_t<GenRasrapRecTile>(t, rl, first, idx, count, out, s);
     case GEN_RASRAP_COUNTER: return points_t<GenRasrapCounter>(t, rl, first, idx, count, out, s);
     case GEN_PHILOX: return points_t<GenPhilox>(t, rl, first, idx, count, out, s);
-    case GEN_SOBOL_GRAY: return points_t<GenSobol<true>>(t, rl, first, idx, count, out, s);
-    case GEN_SOBOL_COUNTER: return points_t<GenSobol<false>>(t, rl, first, idx, count, out, s);
+    case GEN_SOBOL_GRAY:
+      return at ? points_t<GenSobolDirect<true>>(t, rl, first, idx, count, out, s)
+                : points_t<GenSobolTile<true>>(t, rl, first, idx, count, out, s);
+    case GEN_SOBOL_COUNTER:
+      return at ? points_t<GenSobolDirect<false>>(t, rl, first, idx, count, out, s)
+                : points_t<GenSobolTile<false>>(t, rl, first, idx, count, out, s);
     case GEN_SFC64: return points_t<GenSfc64>(t, rl, first, idx, count, out, s);
   }
   return cudaErrorInvalidValue;
@@ -734,11 +970,12 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
   const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
   int blocks = 0;
   switch (a.mp.kind) {
-    case MODEL_LIBOR:
+    case MODEL_LIBOR: {
+      size_t dyn = dyn_bytes(0, a.sig_cap);
 #define RQ_LIBOR_CASE(SS)                                              \
   case SS:                                                             \
-    blocks = persistent_blocks(k_paths_libor<G, SS>, 0, work);         \
-    if (!probe) k_paths_libor<G, SS><<<blocks, TILE, 0, s>>>(a);       \
+    blocks = persistent_blocks(k_paths_libor<G, SS>, dyn, work);       \
+    if (!probe) k_paths_libor<G, SS><<<blocks, TILE, dyn, s>>>(a);     \
     break;
       switch (a.mp.dim) {
         RQ_LIBOR_CASE(10)
@@ -749,16 +986,19 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
       }
 #undef RQ_LIBOR_CASE
       break;
+    }
     case MODEL_MBS: {
-      size_t dyn = sizeof(double) * a.mp.dim;
+      size_t dyn = dyn_bytes(a.mp.dim, a.sig_cap);
       blocks = persistent_blocks(k_paths_mbs<G>, dyn, work);
       if (!probe) k_paths_mbs<G><<<blocks, TILE, dyn, s>>>(a);
       break;
     }
-    case MODEL_X1:
-      blocks = persistent_blocks(k_paths_test<G, false>, 0, work);
-      if (!probe) k_paths_test<G, false><<<blocks, TILE, 0, s>>>(a);
+    case MODEL_X1: {
+      size_t dyn = dyn_bytes(0, a.sig_cap);
+      blocks = persistent_blocks(k_paths_test<G, false>, dyn, work);
+      if (!probe) k_paths_test<G, false><<<blocks, TILE, dyn, s>>>(a);
       break;
+    }
     case MODEL_CONST1:
       blocks = persistent_blocks(k_paths_test<G, true>, 0, work);
       if (!probe) k_paths_test<G, true><<<blocks, TILE, 0, s>>>(a);
@@ -773,11 +1013,11 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
 static cudaError_t paths_dispatch(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                                   int *blocks) {
   switch (a.t.gen) {
-    case GEN_RASRAP_RECURSIVE: return paths_g<GenRasrapRec>(a, launched, s, probe, blocks);
+    case GEN_RASRAP_RECURSIVE: return paths_g<GenRasrapRecTile>(a, launched, s, probe, blocks);
     case GEN_RASRAP_COUNTER: return paths_g<GenRasrapCounter>(a, launched, s, probe, blocks);
     case GEN_PHILOX: return paths_g<GenPhilox>(a, launched, s, probe, blocks);
-    case GEN_SOBOL_GRAY: return paths_g<GenSobol<true>>(a, launched, s, probe, blocks);
-    case GEN_SOBOL_COUNTER: return paths_g<GenSobol<false>>(a, launched, s, probe, blocks);
+    case GEN_SOBOL_GRAY: return paths_g<GenSobolTile<true>>(a, launched, s, probe, blocks);
+    case GEN_SOBOL_COUNTER: return paths_g<GenSobolTile<false>>(a, launched, s, probe, blocks);
     case GEN_SFC64: return paths_g<GenSfc64>(a, launched, s, probe, blocks);
   }
   return cudaErrorInvalidValue;
@@ -793,6 +1033,7 @@ cudaError_t launch_paths(const RepTables &t, const ModelParams &mp, int rep_loca
   a.nmax = nmax;
   a.tiles_per_rep = (nmax + TILE - 1) / TILE;
   a.payoffs = payoffs;
+  a.sig_cap = sig_cap_for(t);
   return paths_dispatch(a, launched, s, false, nullptr);
 }
 
@@ -802,6 +1043,7 @@ int paths_grid_blocks(const RepTables &t, const ModelParams &mp) {
   a.mp = mp;
   a.rep_n = 1 << 20;
   a.tiles_per_rep = 1 << 20;
+  a.sig_cap = sig_cap_for(t);
   int blocks = 0;
   paths_dispatch(a, nullptr, 0, true, &blocks);
   return blocks;
@@ -846,7 +1088,8 @@ cudaError_t launch_inv_normal(const double *u, int64_t n, double *out, cudaStrea
 template <class G>
 static cudaError_t stream_t(const RepTables &t, int rl, int64_t npoints, double *sums,
                             int nblocks, double *store, cudaStream_t s) {
-  k_stream<G><<<nblocks, TILE, 0, s>>>(t, rl, npoints, sums, store);
+  int cap = sig_cap_for(t);
+  k_stream<G><<<nblocks, TILE, dyn_bytes(0, cap), s>>>(t, rl, npoints, sums, store, cap);
   return cudaGetLastError();
 }
 
@@ -854,11 +1097,11 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
                                   double *block_sums, int nblocks, double *store,
                                   cudaStream_t s) {
   switch (t.gen) {
-    case GEN_RASRAP_RECURSIVE: return stream_t<GenRasrapRec>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_RASRAP_RECURSIVE: return stream_t<GenRasrapRecTile>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_RASRAP_COUNTER: return stream_t<GenRasrapCounter>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_PHILOX: return stream_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_SOBOL_GRAY: return stream_t<GenSobol<true>>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_SOBOL_COUNTER: return stream_t<GenSobol<false>>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_SOBOL_GRAY: return stream_t<GenSobolTile<true>>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_SOBOL_COUNTER: return stream_t<GenSobolTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_SFC64: return stream_t<GenSfc64>(t, rl, npoints, block_sums, nblocks, store, s);
   }
   return cudaErrorInvalidValue;

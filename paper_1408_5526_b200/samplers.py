@@ -101,7 +101,7 @@ class DeviceSampler:
 
         lay = halton_layout(self.dim)
         dig = np.empty(((lay["caps"] + 3) & ~3), dtype=np.uint16)
-        sig = np.empty(lay["bases"], dtype=np.float64)
+        sig = np.empty(((lay["bases"] + 3) & ~3), dtype=np.uint16)
         sums = np.empty(lay["sums"], dtype=np.float64)
         _lib.check(_lib.lib().rq_sampler_rasrap_tables(
             self._h, 0, dig.ctypes.data, sig.ctypes.data, sums.ctypes.data))

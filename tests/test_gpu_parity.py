@@ -91,7 +91,7 @@ def test_rasrap_device_tables_match_oracle(P, oracle, tag):
     so = do = 0
     for d in range(dim):
         p, cap = int(lay["base"][d]), int(lay["cap"][d])
-        assert np.array_equal(sig[so:so + p], sigma[d, :p].astype(np.float64))
+        assert np.array_equal(sig[so:so + p], sigma[d, :p])
         n0 = sum(int(a) * p**j for j, a in enumerate(dig[do:do + cap]))
         assert n0 == start[d]
         so += p
