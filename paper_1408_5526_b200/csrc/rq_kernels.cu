@@ -142,7 +142,7 @@ struct RasrapTileShared {
   uint16_t bfull[CHUNK][MAX_CAP];
   int32_t soff[CHUNK];           // sigma offset of the dim (staged or global)
   int32_t lim[CHUNK];            // min(LW, cap)
-  uint16_t scr[LW][TILE];        // per-thread digits of n = B + t
+  uint16_t scr[MAX_CAP][TILE];   // per-thread digits of n = B + t (direct path: all positions)
 };
 struct SobolTileShared {
   uint32_t lowtab[CHUNK][128];   // XOR of v_k over the set bits k < 7
