@@ -127,6 +127,10 @@ const HostTables &host_tables() {
       unsigned __int128 num = ((unsigned __int128)1) << (32 + ell);
       uint64_t m = (uint64_t)((num + p - 1) / p);  // ceil(2^(32+ell)/p) in [2^32, 2^33]
       h.mlo = (uint32_t)m;
+      // 64-bit numerators x < 2^46: q = floor(x * M / 2^(46+ell)) with
+      // M = ceil(2^(46+ell)/p); stored pre-shifted so q = umulhi64(x, m64)
+      unsigned __int128 M = ((((unsigned __int128)1) << (46 + ell)) + p - 1) / p;
+      h.m64 = (uint64_t)(M << (18 - ell));
       h.sig_off = sig;
       h.dig_off = dig;
       h.sum_off = sum;
@@ -365,21 +369,24 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
     size_t b_sig = sizeof(uint16_t) * t.sig_stride * rep_count;
     size_t b_sum = sizeof(double) * t.sum_stride * rep_count;
     size_t b_dig = sizeof(uint16_t) * t.dig_stride * rep_count;
-    cudaError_t e = cudaMallocAsync(&S->mem, b_sig + b_sum + b_dig, s);
+    size_t b_start = sizeof(uint64_t) * dim * rep_count;
+    cudaError_t e = cudaMallocAsync(&S->mem, b_start + b_sig + b_sum + b_dig, s);
     if (e != cudaSuccess) {
       delete S;
       return fail(RQ_ERR_CUDA, "allocating rasrap tables (%zu B): %s", b_sig + b_sum + b_dig,
                   cudaGetErrorString(e));
     }
-    double *sums = (double *)S->mem;
+    uint64_t *start = (uint64_t *)S->mem;
+    double *sums = (double *)(start + (size_t)dim * rep_count);
     uint16_t *sig = (uint16_t *)(sums + t.sum_stride * rep_count);
     uint16_t *dig = sig + t.sig_stride * rep_count;
     t.sigma = sig;
     t.sums = sums;
     t.digits = dig;
+    t.start = start;
     {
       KTimer kt(&g_stats.setup_ms, s);
-      e = rq::launch_rasrap_setup(t, sig, dig, sums, s);
+      e = rq::launch_rasrap_setup(t, sig, dig, sums, start, s);
     }
     if (e != cudaSuccess) {
       cudaFreeAsync(S->mem, s);

@@ -32,6 +32,7 @@ struct HaltonDim {
   int32_t sig_off;  // offset of sigma_d in a replication's sigma block (sum of bases)
   int32_t dig_off;  // offset of the start digits (sum of caps)
   int32_t sum_off;  // offset of partial sums / weight tables (sum of cap+1)
+  uint64_t m64;     // floor(x / base) = umulhi64(x, m64) for x < 2^46
   double inv_p;     // 1.0 / base
   double scale0;    // Python pow(inv_p, K): first init-sum weight (halton.py:274)
 };
@@ -47,6 +48,7 @@ struct RepTables {
   const uint16_t *sigma;   // [rep][sig_stride] digit permutations sigma_d
   const uint16_t *digits;  // [rep][dig_stride] base-p digits of the start index n0
   const double *sums;      // [rep][sum_stride] init partial sums (halton.py:273-278)
+  const uint64_t *start;   // [rep][dim] start indices n0 (invert_radical, halton.py:139-155)
   int64_t sig_stride, dig_stride, sum_stride;
   int32_t sig_chunk_max;   // max over CHUNK-dim groups of the sigma entries they need
   // Sobol
@@ -77,7 +79,7 @@ struct SumPlan {
 cudaError_t upload_halton_dims(const HaltonDim *dims, int n, const double *wts,
                                const double *cscale, int nw);
 cudaError_t launch_rasrap_setup(const RepTables &t, uint16_t *sigma, uint16_t *digits,
-                                double *sums, cudaStream_t s);
+                                double *sums, uint64_t *start, cudaStream_t s);
 cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32_t *gen_v,
                                uint32_t *shift, cudaStream_t s);
 cudaError_t launch_points(const RepTables &t, int rep_local, int64_t first,

@@ -58,7 +58,8 @@ __device__ __forceinline__ uint32_t div_base(uint32_t t, const HaltonDim &h) {
 
 // One thread per (replication, dimension): rasrap_config + RasrapStream
 // init (halton.py:345-360, 256-278, 139-155; seeding.py:59-65).
-__global__ void k_rasrap_setup(RepTables t, uint16_t *sigma, uint16_t *digits, double *sums) {
+__global__ void k_rasrap_setup(RepTables t, uint16_t *sigma, uint16_t *digits, double *sums,
+                               uint64_t *start) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)t.rep_count * t.dim) return;
   int rl = (int)(gid / t.dim), d = (int)(gid % t.dim);
@@ -83,10 +84,14 @@ __global__ void k_rasrap_setup(RepTables t, uint16_t *sigma, uint16_t *digits, d
   uint64_t scaled = (hi << 11) | (lo >> 53);
   uint16_t *dg = digits + (int64_t)rl * t.dig_stride + h.dig_off;
   for (int j = h.K; j < h.cap; j++) dg[j] = 0;
+  uint64_t n0 = 0;
   for (int s = 0; s < h.K; s++) {
-    dg[h.K - 1 - s] = (uint16_t)(scaled % (uint64_t)h.base);
+    uint32_t dgt = (uint32_t)(scaled % (uint64_t)h.base);
+    dg[h.K - 1 - s] = (uint16_t)dgt;
+    n0 = n0 * (uint64_t)h.base + dgt;
     scaled /= (uint64_t)h.base;
   }
+  start[(int64_t)rl * t.dim + d] = n0;
   // init partial sums: scale = pow(1/p, K) then *= p (halton.py:273-278)
   double *sm = sums + (int64_t)rl * t.sum_stride + h.sum_off;
   for (int j = h.K; j <= h.cap; j++) sm[j] = 0.0;
@@ -132,28 +137,35 @@ __global__ void k_sobol_setup(RepTables t, const uint32_t *v, uint32_t *gen_v,
 // "Tiled" generators assume path = base + threadIdx.x (consecutive points);
 // "direct" ones take any path index (sampler.at).
 // ======================================================================
-constexpr int LW = 16;            // low digit window handled per thread (tiled Rasrap)
-constexpr int SIG_SMEM_MAX = 16384;  // u16 sigma entries staged per chunk
+constexpr int LEVBUF = 80;  // nodes per level buffer (>= TILE/2 + 2)
 
 struct RasrapTileShared {
-  double pb[CHUNK][LW + 1];      // stream partial sums at the tile base B, positions 0..LW
-  double wt[CHUNK][LW];          // binpow weights of positions 0..LW-1
-  uint16_t bd[CHUNK][LW];        // base-p digits of B, positions 0..LW-1
-  uint16_t bfull[CHUNK][MAX_CAP];
-  int32_t soff[CHUNK];           // sigma offset of the dim (staged or global)
-  int32_t lim[CHUNK];            // min(LW, cap)
-  uint16_t scr[MAX_CAP][TILE];   // per-thread digits of n = B + t (direct path: all positions)
+  uint16_t bd[CHUNK][MAX_CAP];     // base-p digits of the tile base B = n0 + base
+  int16_t nn[CHUNK][MAX_CAP + 1];  // nodes per level: distinct prefixes floor(n / p^j)
+  int32_t J[CHUNK];                // top level (one node shared by the whole tile)
+  int32_t hB[CHUNK];               // highest digit where B differs from n0 (-1: B == n0)
+  double sJ[CHUNK];                // stream partial sum S_J of the top node
+  double lev[WARPS][2][LEVBUF];    // per-warp ping-pong level buffers
+};
+struct RasrapDirectShared {
+  uint16_t scr[MAX_CAP][TILE];     // per-thread digits (direct path)
 };
 struct SobolTileShared {
-  uint32_t lowtab[CHUNK][128];   // XOR of v_k over the set bits k < 7
-  uint32_t xhi[CHUNK];           // shift ^ XOR of v_k over the tile's bits k >= 7
+  uint32_t lowtab[CHUNK][128];     // XOR of v_k over the set bits k < 7
+  uint32_t xhi[CHUNK];             // shift ^ XOR of v_k over the tile's bits k >= 7
 };
 union GenShared {
   RasrapTileShared r;
+  RasrapDirectShared rd;
   SobolTileShared s;
 };
 
 __device__ __forceinline__ double u16d(uint16_t v) { return (double)v; }
+
+// floor(x / base) for x < 2^46 (64-bit round-up magic, see rq_capi.cu)
+__device__ __forceinline__ uint64_t div_base64(uint64_t x, const HaltonDim &h) {
+  return __umul64hi(x, h.m64);
+}
 
 // Recursive-form point at arbitrary index (Alg. 2, halton.py:392-416)
 // evaluated without replaying the stream: for n = n0 + i let h be the
@@ -196,115 +208,116 @@ struct GenRasrapRecDirect {
     t = &t_;
     rl = rl_;
     i = (uint32_t)path;
-    scr = &sh.r.scr[0][0] + threadIdx.x;
+    scr = &sh.rd.scr[0][0] + threadIdx.x;
   }
-  __device__ void prepare(int, int) {}
-  __device__ void chunk(int d0, int Dc, double *zcol) {
-    for (int dd = 0; dd < Dc; dd++) zcol[dd * TILE] = rasrap_rec_direct(*t, rl, d0 + dd, i, scr);
+  __device__ void fill(int d0, int Dc, double *zt) {
+    for (int dd = 0; dd < Dc; dd++)
+      zt[dd * TILE + threadIdx.x] = rasrap_rec_direct(*t, rl, d0 + dd, i, scr);
   }
 };
 
-// Tiled recursive form.  prepare() builds, per dim of the chunk, the stream
-// state at the tile base B = n0 + base (digits + partial sums P_B[0..LW]);
-// a thread then adds its offset t < TILE to B's low digits and re-chains
-// from P_B[h_t + 1], h_t = highest digit changed by the addition.  This is
-// the same value (above h_t the stream at n equals the stream at B), with
-// ~log_p(TILE) digit positions per point instead of ~log_p(n), and every
-// table access in shared memory.  Carries that run past the window fall
-// back to the direct evaluation.
+// Tiled recursive form, evaluated level by level over the digit tree of the
+// tile's TILE consecutive indices n = B + k, B = n0 + base.
+//
+// With S_j(n) the stream's partial sum at position j for index n, the
+// reference recursion (halton.py:402-414, init sums halton.py:273-278) is
+//     S_j(n) = init_sums[j]                                if floor(n/p^j) == floor(n0/p^j)
+//            = S_{j+1}(n) + sigma(n_j) * binpow(1/p, j+1)   otherwise
+// and S_j only depends on the prefix u = floor(n/p^j).  The tile's indices
+// have N_j distinct prefixes at level j (N_0 = TILE, N_{j+1} = floor((b_j +
+// N_j - 1)/p) + 1 with b_j the digits of B), so the warp owning a dim
+// evaluates the N_j nodes of each level from their parents, top (N_J = 1,
+// whose S_J is the chain from init_sums[hB+1]) to level 0 = the points.
+// That is ~TILE * p/(p-1) node updates per tile and dim instead of
+// TILE * log_p(n) for independent per-point chains, with the same
+// operations in the same order as the reference (bit-identical).
 struct GenRasrapRecTile {
   const RepTables *t;
   int rl;
-  uint32_t base;
+  uint64_t base;
   GenShared *sh;
-  const uint16_t *sig;  // staged (smem) or global sigma of the replication
-  uint16_t *sig_dyn;
-  int sig_cap;
   __device__ void begin(const RepTables &t_, int rl_, uint64_t base_, uint64_t, GenShared &s,
-                        uint16_t *sig_dyn_, int sig_cap_) {
+                        uint16_t *, int) {
     t = &t_;
     rl = rl_;
-    base = (uint32_t)base_;
+    base = base_;
     sh = &s;
-    sig_dyn = sig_dyn_;
-    sig_cap = sig_cap_;
   }
-  __device__ void prepare(int d0, int Dc) {
+  __device__ void fill(int d0, int Dc, double *zt) {
     RasrapTileShared &R = sh->r;
     const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
-    const int off0 = c_hdim[d0].sig_off;
-    const int nsig = c_hdim[d0 + Dc - 1].sig_off + c_hdim[d0 + Dc - 1].base - off0;
-    const bool staged = nsig <= sig_cap;
-    __syncthreads();  // previous chunk is done with the shared state
-    if (staged) {
-      for (int k = threadIdx.x; k < nsig; k += TILE) sig_dyn[k] = gsig[off0 + k];
-      sig = sig_dyn;
-    } else {
-      sig = gsig;
-    }
+    const uint16_t *gdig = t->digits + (int64_t)rl * t->dig_stride;
+    const double *gsum = t->sums + (int64_t)rl * t->sum_stride;
+    __syncthreads();  // previous users of the shared state are done
     if (threadIdx.x < Dc) {
+      // ---- per-dim tile state: digits of B, hB, level sizes, S_J
       const int dd = threadIdx.x;
-      const HaltonDim h = c_hdim[d0 + dd];
+      const HaltonDim &h = c_hdim[d0 + dd];
       const uint32_t p = (uint32_t)h.base;
-      const uint16_t *n0 = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
-      const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
+      const uint16_t *n0d = gdig + h.dig_off;
+      const double *ini = gsum + h.sum_off;
       const uint16_t *sg = gsig + h.sig_off;
       const double *w = g_wts + h.sum_off;
-      // digits of B = n0 + base
-      uint32_t r = base, carry = 0;
-      int hB = -1;
-      for (int j = 0; j < h.cap; j++) {
-        uint32_t q = div_base(r, h);
-        uint32_t a0 = n0[j];
-        uint32_t a = a0 + (r - q * p) + carry;
-        carry = a >= p;
-        a = carry ? a - p : a;
-        R.bfull[dd][j] = (uint16_t)a;
-        hB = (a != a0) ? j : hB;
-        r = q;
+      const uint64_t n0 = t->start[(int64_t)rl * t->dim + d0 + dd];
+      uint64_t qb = n0 + base, qn = n0;
+      int j = 0, hB = -1;
+      while (qb != qn) {  // digits where B's prefix still differs from n0's
+        uint64_t nb = div_base64(qb, h), nq = div_base64(qn, h);
+        uint32_t db = (uint32_t)(qb - nb * p), dn = (uint32_t)(qn - nq * p);
+        R.bd[dd][j] = (uint16_t)db;
+        hB = db != dn ? j : hB;
+        qb = nb;
+        qn = nq;
+        j++;
       }
-      const int lim = LW < h.cap ? LW : h.cap;
-      R.lim[dd] = lim;
-      for (int j = lim; j > hB; j--) R.pb[dd][j] = ini[j];
-      double S = ini[hB + 1];
-      for (int j = hB; j >= 0; j--) {
-        S = dadd(S, dmul(u16d(sg[R.bfull[dd][j]]), w[j]));
-        if (j <= lim) R.pb[dd][j] = S;
+      for (; j < h.cap; j++) R.bd[dd][j] = n0d[j];
+      int N = TILE, J = 0;
+      R.nn[dd][0] = (int16_t)N;
+      while (N > 1) {
+        N = (int)div_base((uint32_t)R.bd[dd][J] + (uint32_t)N - 1u, h) + 1;
+        J++;
+        R.nn[dd][J] = (int16_t)N;
       }
-      for (int j = 0; j < lim; j++) {
-        R.bd[dd][j] = R.bfull[dd][j];
-        R.wt[dd][j] = w[j];
-      }
-      R.soff[dd] = staged ? h.sig_off - off0 : h.sig_off;
+      double S = ini[hB + 1 > J ? hB + 1 : J];
+      for (int k = hB; k >= J; k--) S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
+      R.J[dd] = J;
+      R.hB[dd] = hB;
+      R.sJ[dd] = S;
     }
     __syncthreads();
-  }
-  __device__ __forceinline__ double value(int d, int dd) const {
-    const RasrapTileShared &R = sh->r;
-    const uint32_t p = (uint32_t)c_hdim[d].base;
-    const int lim = R.lim[dd];
-    uint16_t *scr = const_cast<uint16_t *>(&R.scr[0][0]) + threadIdx.x;
-    uint32_t r = threadIdx.x, carry = 0;
-    int h = -1, j = 0;
-    while (r != 0u || carry != 0u) {
-      if (j >= lim) return rasrap_rec_direct(*t, rl, d, base + threadIdx.x, scr);
-      uint32_t q = div_base(r, c_hdim[d]);
-      uint32_t b = R.bd[dd][j];
-      uint32_t a = b + (r - q * p) + carry;
-      carry = a >= p;
-      a = carry ? a - p : a;
-      scr[j * TILE] = (uint16_t)a;
-      h = (a != b) ? j : h;
-      r = q;
-      j++;
+    // ---- warp-cooperative descent of the digit tree, one dim at a time
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int dd = warp; dd < Dc; dd += WARPS) {
+      const HaltonDim &h = c_hdim[d0 + dd];
+      const uint32_t p = (uint32_t)h.base;
+      const uint16_t *sg = gsig + h.sig_off;
+      const double *ini = gsum + h.sum_off;
+      const double *w = g_wts + h.sum_off;
+      const int J = R.J[dd], hB = R.hB[dd];
+      double *prev = R.lev[warp][0], *next = R.lev[warp][1];
+      if (lane == 0) prev[0] = R.sJ[dd];
+      __syncwarp();
+      for (int j = J - 1; j >= 0; j--) {
+        const int Nj = R.nn[dd][j];
+        const uint32_t bj = R.bd[dd][j];
+        const double wj = w[j], inij = ini[j];
+        const bool at_n0 = j > hB;  // node 0 of this level has n0's prefix
+        double *dst = j ? next : zt + dd * TILE;
+        for (int k = lane; k < Nj; k += 32) {
+          const uint32_t x = bj + (uint32_t)k;
+          const uint32_t par = div_base(x, h);
+          const uint32_t a = x - par * p;
+          double v = dadd(prev[par], dmul(u16d(sg[a]), wj));
+          dst[k] = (at_n0 && k == 0) ? inij : v;
+        }
+        __syncwarp();
+        double *tmp = prev;
+        prev = next;
+        next = tmp;
+      }
+      if (J == 0 && lane == 0) zt[dd * TILE] = R.sJ[dd];  // unreachable: TILE > 1
     }
-    const uint16_t *sg = sig + R.soff[dd];
-    double S = R.pb[dd][h + 1];
-    for (int k = h; k >= 0; k--) S = dadd(S, dmul(u16d(sg[scr[k * TILE]]), R.wt[dd][k]));
-    return S;
-  }
-  __device__ void chunk(int d0, int Dc, double *zcol) {
-    for (int dd = 0; dd < Dc; dd++) zcol[dd * TILE] = value(d0 + dd, dd);
+    __syncthreads();
   }
 };
 
@@ -320,7 +333,6 @@ struct GenRasrapCounter {
     dig = t.digits + (int64_t)rl * t.dig_stride;
     i = (uint32_t)path;
   }
-  __device__ void prepare(int, int) {}
   __device__ __forceinline__ double value(int d) const {
     const HaltonDim &h = c_hdim[d];
     const uint16_t *d0 = dig + h.dig_off;
@@ -338,8 +350,8 @@ struct GenRasrapCounter {
     }
     return x;
   }
-  __device__ void chunk(int d0, int Dc, double *zcol) {
-    for (int dd = 0; dd < Dc; dd++) zcol[dd * TILE] = value(d0 + dd);
+  __device__ void fill(int d0, int Dc, double *zt) {
+    for (int dd = 0; dd < Dc; dd++) zt[dd * TILE + threadIdx.x] = value(d0 + dd);
   }
 };
 
@@ -355,8 +367,8 @@ struct GenPhilox {
     plo = (uint32_t)path;
     phi = (uint32_t)(path >> 32);
   }
-  __device__ void prepare(int, int) {}
-  __device__ void chunk(int d0, int Dc, double *zcol) {  // d0 % 4 == 0
+  __device__ void fill(int d0, int Dc, double *zt) {  // d0 % 4 == 0
+    double *zcol = zt + threadIdx.x;
     for (int dd = 0; dd < Dc; dd += 4) {
       U4 w = philox4x32_10((uint32_t)((d0 + dd) >> 2), plo, phi, 0u, k0, k1);
       const double s = 2.3283064365386963e-10, hlf = 1.1641532182693481e-10;
@@ -381,8 +393,8 @@ struct GenSobolDirect {
     shift = t.sobol_shift + (int64_t)rl * t.dim;
     idx = GRAY ? (path ^ (path >> 1)) : path;
   }
-  __device__ void prepare(int, int) {}
-  __device__ void chunk(int d0, int Dc, double *zcol) {
+  __device__ void fill(int d0, int Dc, double *zt) {
+    double *zcol = zt + threadIdx.x;
     for (int dd = 0; dd < Dc; dd++) {
       const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
       uint32_t x = __ldg(shift + d0 + dd);
@@ -441,7 +453,9 @@ struct GenSobolTile {
     }
     __syncthreads();
   }
-  __device__ void chunk(int d0, int Dc, double *zcol) {
+  __device__ void fill(int d0, int Dc, double *zt) {
+    prepare(d0, Dc);
+    double *zcol = zt + threadIdx.x;
     const SobolTileShared &S = sh->s;
     for (int dd = 0; dd < Dc; dd++) {
       uint32_t x;
@@ -467,10 +481,9 @@ struct GenSfc64 {
     uint64_t km = derive_key3(t.seed, 7, (uint64_t)(t.rep_first + rl));
     sfc_seed(s, splitmix64(km ^ path));
   }
-  __device__ void prepare(int, int) {}
-  __device__ void chunk(int d0, int Dc, double *zcol) {
+  __device__ void fill(int d0, int Dc, double *zt) {
     for (int dd = 0; dd < Dc; dd++)
-      zcol[dd * TILE] = (double)(sfc_next(s) >> 11) * (1.0 / 9007199254740992.0);
+      zt[dd * TILE + threadIdx.x] = (double)(sfc_next(s) >> 11) * (1.0 / 9007199254740992.0);
   }
 };
 
@@ -629,8 +642,7 @@ __global__ void __launch_bounds__(TILE) k_paths_libor(PathArgs a) {
     md.begin(a.mp, l0s);
     for (int d0 = 0; d0 < S; d0 += CHUNK) {
       const int Dc = S - d0 < CHUNK ? S - d0 : CHUNK;
-      g.prepare(d0, Dc);
-      g.chunk(d0, Dc, zt + threadIdx.x);
+      g.fill(d0, Dc, zt);
       __syncwarp();
       chunk_to_normals(zt, Dc, tq[warp]);
       md.chunk(d0, Dc, zt + threadIdx.x, TILE);
@@ -663,8 +675,7 @@ __global__ void __launch_bounds__(TILE) k_paths_mbs(PathArgs a) {
     md.begin(a.mp, cks);
     for (int d0 = 0; d0 < a.mp.dim; d0 += CHUNK) {
       const int Dc = a.mp.dim - d0 < CHUNK ? a.mp.dim - d0 : CHUNK;
-      g.prepare(d0, Dc);
-      g.chunk(d0, Dc, zt + threadIdx.x);
+      g.fill(d0, Dc, zt);
       __syncwarp();
       chunk_to_normals(zt, Dc, tq[warp]);
       md.chunk(d0, Dc, zt + threadIdx.x, TILE, a.mp);
@@ -690,8 +701,7 @@ __global__ void __launch_bounds__(TILE) k_paths_test(PathArgs a) {
     if (!CONST1) {
       G g;
       g.begin(a.t, rl, (uint64_t)base, (uint64_t)path, gsh, sig_dyn, a.sig_cap);
-      g.prepare(0, 1);
-      g.chunk(0, 1, zt + threadIdx.x);
+      g.fill(0, 1, zt);
       f = zt[threadIdx.x];
     }
     if (path < a.nmax) a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = f;
@@ -718,8 +728,7 @@ __global__ void __launch_bounds__(TILE) k_points(RepTables t, int rl, int64_t fi
     g.begin(t, rl, (uint64_t)(first + tb), (uint64_t)path, gsh, sig_dyn, sig_cap);
     for (int d0 = 0; d0 < t.dim; d0 += CHUNK) {
       const int Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
-      g.prepare(d0, Dc);
-      g.chunk(d0, Dc, zt + threadIdx.x);
+      g.fill(d0, Dc, zt);
       if (ok)
         for (int dd = 0; dd < Dc; dd++) out[r * t.dim + d0 + dd] = zt[dd * TILE + threadIdx.x];
     }
@@ -837,8 +846,7 @@ __global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t np
     g.begin(t, rl, (uint64_t)tb, (uint64_t)r, gsh, sig_dyn, sig_cap);
     for (int d0 = 0; d0 < t.dim; d0 += CHUNK) {
       const int Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
-      g.prepare(d0, Dc);
-      g.chunk(d0, Dc, zt + threadIdx.x);
+      g.fill(d0, Dc, zt);
       __syncwarp();
       chunk_to_normals(zt, Dc, tq[warp]);
       if (ok) {
@@ -911,10 +919,10 @@ static int persistent_blocks(K kernel, size_t dyn_smem, int64_t work) {
 }
 
 cudaError_t launch_rasrap_setup(const RepTables &t, uint16_t *sigma, uint16_t *digits,
-                                double *sums, cudaStream_t s) {
+                                double *sums, uint64_t *start, cudaStream_t s) {
   int64_t n = (int64_t)t.rep_count * t.dim;
   int blocks = (int)((n + 127) / 128);
-  k_rasrap_setup<<<blocks, 128, 0, s>>>(t, sigma, digits, sums);
+  k_rasrap_setup<<<blocks, 128, 0, s>>>(t, sigma, digits, sums, start);
   return cudaGetLastError();
 }
 
@@ -926,9 +934,8 @@ cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32
   return cudaGetLastError();
 }
 
-static int sig_cap_for(const RepTables &t) {
-  return (t.gen == GEN_RASRAP_RECURSIVE && t.sig_chunk_max <= SIG_SMEM_MAX) ? t.sig_chunk_max : 0;
-}
+// sigma tables are read from global (L1-resident); no staging
+static int sig_cap_for(const RepTables &) { return 0; }
 static size_t dyn_bytes(int table_doubles, int sig_cap) {
   return sizeof(double) * table_doubles + sizeof(uint16_t) * sig_cap;
 }
