@@ -1,23 +1,24 @@
 // rq_kernels.cu -- sm_100a kernels of the RQMC estimator.
 //
-// Layout of the fused path kernel (one CTA = one tile of T consecutive
-// paths of one replication, persistent over (replication, tile) work items):
+// Fused path kernel (k_paths): one CTA owns a tile of TILE consecutive paths
+// of one replication and walks its tiles (persistent, grid-stride) in units
+// of (tile, chunk of CHUNK dimensions).  Per unit:
 //
-//   for each chunk of D dimensions (Euler steps / months):
-//     1. generator: every thread writes the D uniforms of ITS path into a
-//        shared-memory column zt[dd][tid]            (no HBM traffic)
-//     2. inverse normal, warp-cooperative: central branch inline, the ~9%
-//        tail inputs are compacted into a per-warp queue and evaluated 32
-//        at a time (no log/sqrt divergence in the common branch)
-//     3. model: the thread advances its path state (forward rates / MBS
-//        cash-flow state) in registers through the D steps
-//   payoff -> payoffs[rep][path]  (8 B/path, the only HBM write)
+//   generator   uniforms of the unit into a shared-memory tile zt[dd][t]
+//               (Rasrap / Sobol': warp w builds the rows dd = w (mod WARPS)
+//               for all TILE points; PRNGs: every thread its own column)
+//   normals     warp-cooperative inverse normal of the thread's own column:
+//               central branch inline, the ~9% tail inputs compacted into a
+//               per-warp queue and evaluated 32 at a time
+//   model       thread-per-path state in registers (forward rates / MBS
+//               cash-flow state) advanced through the chunk's steps
 //
-// then k_reduce applies numpy's pairwise-summation tree to each
-// replication's payoff prefix (bit-identical to the reference np.sum).
-//
-// Every warp only touches its own shared-memory columns, so the tile loop
-// needs __syncwarp only -- no CTA barriers on the hot path.
+// The generator of unit u+1 runs in the same iteration as normals+model of
+// unit u on the other half of a double-buffered tile, so the warps' uneven
+// generator work is absorbed by model work; one __syncthreads per unit.
+// The payoff (8 B/path) is the only HBM write; k_reduce then applies
+// numpy's pairwise-summation tree to each replication's payoff prefix
+// (bit-identical to the reference np.sum).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,9 +28,12 @@
 
 namespace rq {
 
-constexpr int TILE = 128;  // paths per CTA tile = threads per CTA
-constexpr int CHUNK = CHUNK_DIMS;  // dimensions per generator chunk (multiple of 4 for Philox)
+constexpr int TILE = 128;          // paths per CTA tile = threads per CTA
+constexpr int CHUNK = CHUNK_DIMS;  // dimensions per unit (multiple of 4 for Philox)
 constexpr int WARPS = TILE / 32;
+constexpr double TWO_M32 = 2.3283064365386963e-10;  // 2^-32
+constexpr double TWO_M33 = 1.1641532182693481e-10;  // 2^-33
+constexpr double TWO_M53 = 1.1102230246251565e-16;  // 2^-53
 
 __constant__ HaltonDim c_hdim[MAX_DIM];
 constexpr int WTS_CAP = 16384;
@@ -51,6 +55,11 @@ __device__ __forceinline__ uint32_t div_base(uint32_t t, const HaltonDim &h) {
   uint64_t x = (uint64_t)__umulhi(t, h.mlo) + t;
   return (uint32_t)(x >> h.ell);
 }
+// floor(x / base) for x < 2^46 (64-bit round-up magic, see rq_capi.cu)
+__device__ __forceinline__ uint64_t div_base64(uint64_t x, const HaltonDim &h) {
+  return __umul64hi(x, h.m64);
+}
+__device__ __forceinline__ double u16d(uint16_t v) { return (double)v; }
 
 // ======================================================================
 // Setup kernels (per replication randomisation, on device)
@@ -129,13 +138,12 @@ __global__ void k_sobol_setup(RepTables t, const uint32_t *v, uint32_t *gen_v,
 }
 
 // ======================================================================
-// Generators.  Every thread produces the uniforms of ITS point for dims
-// [d0, d0+Dc) into a shared-memory column (stride TILE).  Interface:
-//   begin(t, rl, base, path, sh, sig_dyn, sig_cap)  per thread
-//   prepare(d0, Dc)   block-cooperative (all threads, may __syncthreads)
-//   chunk(d0, Dc, zcol)
-// "Tiled" generators assume path = base + threadIdx.x (consecutive points);
-// "direct" ones take any path index (sampler.at).
+// Generators.  unit(rl, base, path, d0, Dc, zt) writes the uniforms of
+// points base..base+TILE-1 (this thread's: path) for dims [d0, d0+Dc) into
+// zt[dd*TILE + t].  It is warp-synchronous (no CTA barrier inside), so the
+// caller can overlap it with other warps' model work.  "Tiled" generators
+// require path == base + threadIdx.x; "direct" ones take any index
+// (sampler.at).
 // ======================================================================
 constexpr int LEVBUF = 80;  // nodes per level buffer (>= TILE/2 + 2)
 
@@ -148,31 +156,18 @@ struct RasrapTileShared {
   double lev[WARPS][2][LEVBUF];    // per-warp ping-pong level buffers
 };
 struct RasrapDirectShared {
-  uint16_t scr[MAX_CAP][TILE];     // per-thread digits (direct path)
+  uint16_t scr[MAX_CAP][TILE];  // per-thread digits (direct path)
 };
-struct SobolTileShared {
-  uint32_t lowtab[CHUNK][128];     // XOR of v_k over the set bits k < 7
-  uint32_t xhi[CHUNK];             // shift ^ XOR of v_k over the tile's bits k >= 7
-};
-union GenShared {
-  RasrapTileShared r;
-  RasrapDirectShared rd;
-  SobolTileShared s;
+struct NoShared {
+  int unused;
 };
 
-__device__ __forceinline__ double u16d(uint16_t v) { return (double)v; }
-
-// floor(x / base) for x < 2^46 (64-bit round-up magic, see rq_capi.cu)
-__device__ __forceinline__ uint64_t div_base64(uint64_t x, const HaltonDim &h) {
-  return __umul64hi(x, h.m64);
-}
-
-// Recursive-form point at arbitrary index (Alg. 2, halton.py:392-416)
-// evaluated without replaying the stream: for n = n0 + i let h be the
-// highest digit where n and n0 differ (= highest carry the odometer
-// reached).  The stream then holds sums[j] = init_sums[j] above h and the
-// chain S_j = S_{j+1} + sigma(a_j) * binpow(1/p, j+1) below, so the point is
-// that chain started from init_sums[h+1] -- bit-identical to the reference.
+// Recursive-form point at an arbitrary index (Alg. 2, halton.py:392-416)
+// without replaying the stream: for n = n0 + i let h be the highest digit
+// where n and n0 differ (= highest carry the odometer reached).  The stream
+// then holds sums[j] = init_sums[j] above h and the chain
+// S_j = S_{j+1} + sigma(a_j) * binpow(1/p, j+1) below, so the point is that
+// chain started from init_sums[h+1] -- bit-identical to the reference.
 __device__ double rasrap_rec_direct(const RepTables &t, int rl, int d, uint32_t i,
                                     uint16_t *scr) {
   const HaltonDim &h = c_hdim[d];
@@ -199,20 +194,17 @@ __device__ double rasrap_rec_direct(const RepTables &t, int rl, int d, uint32_t 
 }
 
 struct GenRasrapRecDirect {
+  using Shared = RasrapDirectShared;
   const RepTables *t;
-  int rl;
-  uint32_t i;
-  uint16_t *scr;
-  __device__ void begin(const RepTables &t_, int rl_, uint64_t, uint64_t path, GenShared &sh,
-                        uint16_t *, int) {
+  Shared *sh;
+  __device__ void setup(const RepTables &t_, Shared &s) {
     t = &t_;
-    rl = rl_;
-    i = (uint32_t)path;
-    scr = &sh.rd.scr[0][0] + threadIdx.x;
+    sh = &s;
   }
-  __device__ void fill(int d0, int Dc, double *zt) {
+  __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
+    uint16_t *scr = &sh->scr[0][0] + threadIdx.x;
     for (int dd = 0; dd < Dc; dd++)
-      zt[dd * TILE + threadIdx.x] = rasrap_rec_direct(*t, rl, d0 + dd, i, scr);
+      zt[dd * TILE + threadIdx.x] = rasrap_rec_direct(*t, rl, d0 + dd, (uint32_t)path, scr);
   }
 };
 
@@ -221,8 +213,8 @@ struct GenRasrapRecDirect {
 //
 // With S_j(n) the stream's partial sum at position j for index n, the
 // reference recursion (halton.py:402-414, init sums halton.py:273-278) is
-//     S_j(n) = init_sums[j]                                if floor(n/p^j) == floor(n0/p^j)
-//            = S_{j+1}(n) + sigma(n_j) * binpow(1/p, j+1)   otherwise
+//     S_j(n) = init_sums[j]                               if floor(n/p^j) == floor(n0/p^j)
+//            = S_{j+1}(n) + sigma(n_j) * binpow(1/p, j+1)  otherwise
 // and S_j only depends on the prefix u = floor(n/p^j).  The tile's indices
 // have N_j distinct prefixes at level j (N_0 = TILE, N_{j+1} = floor((b_j +
 // N_j - 1)/p) + 1 with b_j the digits of B), so the warp owning a dim
@@ -232,61 +224,59 @@ struct GenRasrapRecDirect {
 // TILE * log_p(n) for independent per-point chains, with the same
 // operations in the same order as the reference (bit-identical).
 struct GenRasrapRecTile {
+  using Shared = RasrapTileShared;
   const RepTables *t;
-  int rl;
-  uint64_t base;
-  GenShared *sh;
-  __device__ void begin(const RepTables &t_, int rl_, uint64_t base_, uint64_t, GenShared &s,
-                        uint16_t *, int) {
+  Shared *sh;
+  __device__ void setup(const RepTables &t_, Shared &s) {
     t = &t_;
-    rl = rl_;
-    base = base_;
     sh = &s;
   }
-  __device__ void fill(int d0, int Dc, double *zt) {
-    RasrapTileShared &R = sh->r;
-    const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
-    const uint16_t *gdig = t->digits + (int64_t)rl * t->dig_stride;
-    const double *gsum = t->sums + (int64_t)rl * t->sum_stride;
-    __syncthreads();  // previous users of the shared state are done
-    if (threadIdx.x < Dc) {
-      // ---- per-dim tile state: digits of B, hB, level sizes, S_J
-      const int dd = threadIdx.x;
-      const HaltonDim &h = c_hdim[d0 + dd];
-      const uint32_t p = (uint32_t)h.base;
-      const uint16_t *n0d = gdig + h.dig_off;
-      const double *ini = gsum + h.sum_off;
-      const uint16_t *sg = gsig + h.sig_off;
-      const double *w = g_wts + h.sum_off;
-      const uint64_t n0 = t->start[(int64_t)rl * t->dim + d0 + dd];
-      uint64_t qb = n0 + base, qn = n0;
-      int j = 0, hB = -1;
-      while (qb != qn) {  // digits where B's prefix still differs from n0's
-        uint64_t nb = div_base64(qb, h), nq = div_base64(qn, h);
-        uint32_t db = (uint32_t)(qb - nb * p), dn = (uint32_t)(qn - nq * p);
-        R.bd[dd][j] = (uint16_t)db;
-        hB = db != dn ? j : hB;
-        qb = nb;
-        qn = nq;
-        j++;
-      }
-      for (; j < h.cap; j++) R.bd[dd][j] = n0d[j];
-      int N = TILE, J = 0;
-      R.nn[dd][0] = (int16_t)N;
-      while (N > 1) {
-        N = (int)div_base((uint32_t)R.bd[dd][J] + (uint32_t)N - 1u, h) + 1;
-        J++;
-        R.nn[dd][J] = (int16_t)N;
-      }
-      double S = ini[hB + 1 > J ? hB + 1 : J];
-      for (int k = hB; k >= J; k--) S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
-      R.J[dd] = J;
-      R.hB[dd] = hB;
-      R.sJ[dd] = S;
+  // per-dim tile state (one lane per dim): digits of B, hB, level sizes, S_J
+  __device__ void prepare_dim(int rl, uint64_t base, int d, int dd) {
+    RasrapTileShared &R = *sh;
+    const HaltonDim &h = c_hdim[d];
+    const uint32_t p = (uint32_t)h.base;
+    const uint16_t *n0d = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
+    const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
+    const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
+    const double *w = g_wts + h.sum_off;
+    const uint64_t n0 = t->start[(int64_t)rl * t->dim + d];
+    uint64_t qb = n0 + base, qn = n0;
+    int j = 0, hB = -1;
+    while (qb != qn) {  // positions where B's prefix still differs from n0's
+      uint64_t nb = div_base64(qb, h), nq = div_base64(qn, h);
+      uint32_t db = (uint32_t)(qb - nb * p), dn = (uint32_t)(qn - nq * p);
+      R.bd[dd][j] = (uint16_t)db;
+      hB = db != dn ? j : hB;
+      qb = nb;
+      qn = nq;
+      j++;
     }
-    __syncthreads();
-    // ---- warp-cooperative descent of the digit tree, one dim at a time
+    int N = TILE, J = 0;
+    R.nn[dd][0] = (int16_t)N;
+    while (N > 1) {
+      uint32_t bj = J < j ? R.bd[dd][J] : n0d[J];
+      if (J >= j) R.bd[dd][J] = (uint16_t)bj;
+      N = (int)div_base(bj + (uint32_t)N - 1u, h) + 1;
+      J++;
+      R.nn[dd][J] = (int16_t)N;
+    }
+    double S = ini[hB + 1 > J ? hB + 1 : J];
+    for (int k = hB; k >= J; k--) S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
+    R.J[dd] = J;
+    R.hB[dd] = hB;
+    R.sJ[dd] = S;
+  }
+  __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
+    RasrapTileShared &R = *sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {  // lane k prepares dim dd = warp + k * WARPS
+      const int dd = warp + lane * WARPS;
+      if (dd < Dc) prepare_dim(rl, base, d0 + dd, dd);
+    }
+    __syncwarp();
+    const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
+    const double *gsum = t->sums + (int64_t)rl * t->sum_stride;
     for (int dd = warp; dd < Dc; dd += WARPS) {
       const HaltonDim &h = c_hdim[d0 + dd];
       const uint32_t p = (uint32_t)h.base;
@@ -315,204 +305,195 @@ struct GenRasrapRecTile {
         prev = next;
         next = tmp;
       }
-      if (J == 0 && lane == 0) zt[dd * TILE] = R.sJ[dd];  // unreachable: TILE > 1
     }
-    __syncthreads();
   }
 };
 
 // Rasrap counter form (Alg. 3, halton.py:419-440): sum sigma(a_j)*scale_j
 // from the least significant digit up, scale_j = (1/p)^(j+1) by repeated
-// multiplication, over max(K, #digits) positions.
+// multiplication, over max(K, #digits) positions.  The running sum starts
+// at the low digits, so no prefix can be shared across a tile: direct.
 struct GenRasrapCounter {
-  const uint16_t *sig, *dig;
-  uint32_t i;
-  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
-                        uint16_t *, int) {
-    sig = t.sigma + (int64_t)rl * t.sig_stride;
-    dig = t.digits + (int64_t)rl * t.dig_stride;
-    i = (uint32_t)path;
-  }
-  __device__ __forceinline__ double value(int d) const {
+  const RepTables *t;
+  using Shared = NoShared;
+  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ __forceinline__ double value(int rl, int d, uint32_t i) const {
     const HaltonDim &h = c_hdim[d];
-    const uint16_t *d0 = dig + h.dig_off;
-    const uint16_t *sg = sig + h.sig_off;
+    const uint16_t *d0 = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
+    const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
     const double *cs = g_cscale + h.sum_off;
-    uint32_t t = i, carry = 0;
+    uint32_t r = i, carry = 0;
     double x = 0.0;
-    for (int j = 0; j < h.K || t != 0u || carry != 0u; j++) {
-      uint32_t q = div_base(t, h);
-      uint32_t a = d0[j] + (t - q * (uint32_t)h.base) + carry;
+    for (int j = 0; j < h.K || r != 0u || carry != 0u; j++) {
+      uint32_t q = div_base(r, h);
+      uint32_t a = d0[j] + (r - q * (uint32_t)h.base) + carry;
       carry = a >= (uint32_t)h.base;
       a = carry ? a - (uint32_t)h.base : a;
       x = dadd(x, dmul(u16d(sg[a]), cs[j]));
-      t = q;
+      r = q;
     }
     return x;
   }
-  __device__ void fill(int d0, int Dc, double *zt) {
-    for (int dd = 0; dd < Dc; dd++) zt[dd * TILE + threadIdx.x] = value(d0 + dd);
+  __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
+    for (int dd = 0; dd < Dc; dd++)
+      zt[dd * TILE + threadIdx.x] = value(rl, d0 + dd, (uint32_t)path);
   }
 };
 
-// Philox-4x32-10, counter (b, path_lo, path_hi, 0), u = (w + 1/2) 2^-32
+// Philox-4x32-10, counter (b, path_lo, path_hi, 0), u = w 2^-32 + 2^-33
 // (prng.py:180-231, harness.py:53-67).
 struct GenPhilox {
-  uint32_t k0, k1, plo, phi;
-  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
-                        uint16_t *, int) {
-    uint64_t key = derive_key3(t.seed, 3, (uint64_t)(t.rep_first + rl));
-    k0 = (uint32_t)key;
-    k1 = (uint32_t)(key >> 32);
-    plo = (uint32_t)path;
-    phi = (uint32_t)(path >> 32);
-  }
-  __device__ void fill(int d0, int Dc, double *zt) {  // d0 % 4 == 0
+  const RepTables *t;
+  using Shared = NoShared;
+  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
+    const uint64_t key = derive_key3(t->seed, 3, (uint64_t)(t->rep_first + rl));
+    const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
     double *zcol = zt + threadIdx.x;
-    for (int dd = 0; dd < Dc; dd += 4) {
-      U4 w = philox4x32_10((uint32_t)((d0 + dd) >> 2), plo, phi, 0u, k0, k1);
-      const double s = 2.3283064365386963e-10, hlf = 1.1641532182693481e-10;
-      zcol[dd * TILE] = (double)w.x * s + hlf;
-      if (dd + 1 < Dc) zcol[(dd + 1) * TILE] = (double)w.y * s + hlf;
-      if (dd + 2 < Dc) zcol[(dd + 2) * TILE] = (double)w.z * s + hlf;
-      if (dd + 3 < Dc) zcol[(dd + 3) * TILE] = (double)w.w * s + hlf;
+    for (int dd = 0; dd < Dc; dd += 4) {  // d0 % 4 == 0
+      U4 w = philox4x32_10((uint32_t)((d0 + dd) >> 2), (uint32_t)path, (uint32_t)(path >> 32),
+                           0u, k0, k1);
+      zcol[dd * TILE] = (double)w.x * TWO_M32 + TWO_M33;
+      if (dd + 1 < Dc) zcol[(dd + 1) * TILE] = (double)w.y * TWO_M32 + TWO_M33;
+      if (dd + 2 < Dc) zcol[(dd + 2) * TILE] = (double)w.z * TWO_M32 + TWO_M33;
+      if (dd + 3 < Dc) zcol[(dd + 3) * TILE] = (double)w.w * TWO_M32 + TWO_M33;
     }
   }
 };
 
-// Scrambled Sobol' (sobol.py:313-372): point at index j is the XOR of the
-// pre-scrambled direction words over the set bits of j, XOR the shift;
-// the Gray-code sampler's point i is the counter point at i ^ (i >> 1).
+// Scrambled Sobol' (sobol.py:313-372): the point at counter index j is the
+// XOR of the pre-scrambled direction words over the set bits of j, XOR the
+// shift; the Gray-code sampler's point i is the counter point at i^(i>>1).
+template <bool GRAY>
+__device__ __forceinline__ uint32_t sobol_word(const uint32_t *vd, uint32_t shift, uint64_t i) {
+  uint32_t x = shift;
+  uint32_t bits = (uint32_t)(GRAY ? (i ^ (i >> 1)) : i);
+  for (; bits; bits &= bits - 1u) x ^= vd[__ffs(bits) - 1];
+  return x;
+}
+
 template <bool GRAY>
 struct GenSobolDirect {
-  const uint32_t *v, *shift;
-  uint64_t idx;
-  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
-                        uint16_t *, int) {
-    v = t.sobol_v + (int64_t)rl * t.dim * SOBOL_BITS;
-    shift = t.sobol_shift + (int64_t)rl * t.dim;
-    idx = GRAY ? (path ^ (path >> 1)) : path;
-  }
-  __device__ void fill(int d0, int Dc, double *zt) {
-    double *zcol = zt + threadIdx.x;
-    for (int dd = 0; dd < Dc; dd++) {
-      const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
-      uint32_t x = __ldg(shift + d0 + dd);
-      uint32_t bits = (uint32_t)idx;
-      while (bits) {
-        int k = __ffs(bits) - 1;
-        x ^= __ldg(vd + k);
-        bits &= bits - 1u;
-      }
-      zcol[dd * TILE] = (double)x * 2.3283064365386963e-10;
-    }
+  const RepTables *t;
+  using Shared = NoShared;
+  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
+    const uint32_t *v = t->sobol_v + (int64_t)rl * t->dim * SOBOL_BITS;
+    const uint32_t *sh = t->sobol_shift + (int64_t)rl * t->dim;
+    for (int dd = 0; dd < Dc; dd++)
+      zt[dd * TILE + threadIdx.x] =
+          (double)sobol_word<GRAY>(v + (d0 + dd) * SOBOL_BITS, sh[d0 + dd], path) * TWO_M32;
   }
 };
 
-// Tiled Sobol': the index bits >= 7 are shared by a 128-aligned tile, so
-// prepare() folds them (and the shift) into one word per dim and tabulates
-// the 128 low-bit XOR patterns; a point is then one table lookup.  Tiles
-// that are not 128-aligned (sampler.fill from an odd start) take the
-// direct loop.
+// Tiled Sobol': in a 128-aligned tile the index bits >= 7 are common, so
+// the warp owning a dim folds them and the shift into one word; each point
+// then XORs at most 7 more direction words.  Unaligned tiles (sampler.fill
+// from an odd start) use the per-point loop.
 template <bool GRAY>
 struct GenSobolTile {
-  const uint32_t *v, *shift;
-  uint32_t idx, hi_key;
-  bool aligned;
-  GenShared *sh;
-  __device__ void begin(const RepTables &t, int rl, uint64_t base, uint64_t path, GenShared &s,
-                        uint16_t *, int) {
-    v = t.sobol_v + (int64_t)rl * t.dim * SOBOL_BITS;
-    shift = t.sobol_shift + (int64_t)rl * t.dim;
-    uint32_t i = (uint32_t)path, b = (uint32_t)base;
-    idx = GRAY ? (i ^ (i >> 1)) : i;
-    uint32_t bidx = GRAY ? (b ^ (b >> 1)) : b;
-    hi_key = bidx >> 7;
-    aligned = (b & 127u) == 0u;
-    sh = &s;
-  }
-  __device__ void prepare(int d0, int Dc) {
-    SobolTileShared &S = sh->s;
-    __syncthreads();
-    if (aligned) {
-      for (int e = threadIdx.x; e < Dc * 128; e += TILE) {
-        int dd = e >> 7, x = e & 127;
-        const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
-        uint32_t acc = 0;
-        for (int k = 0; k < 7; k++)
-          if (x & (1 << k)) acc ^= vd[k];
-        S.lowtab[dd][x] = acc;
-      }
-      if (threadIdx.x < Dc) {
-        const uint32_t *vd = v + (d0 + threadIdx.x) * SOBOL_BITS;
-        uint32_t acc = shift[d0 + threadIdx.x], bits = hi_key;
-        for (int k = 7; bits; k++, bits >>= 1)
-          if (bits & 1u) acc ^= vd[k];
-        S.xhi[threadIdx.x] = acc;
-      }
-    }
-    __syncthreads();
-  }
-  __device__ void fill(int d0, int Dc, double *zt) {
-    prepare(d0, Dc);
-    double *zcol = zt + threadIdx.x;
-    const SobolTileShared &S = sh->s;
-    for (int dd = 0; dd < Dc; dd++) {
-      uint32_t x;
+  const RepTables *t;
+  using Shared = NoShared;
+  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
+    const uint32_t *v = t->sobol_v + (int64_t)rl * t->dim * SOBOL_BITS;
+    const uint32_t *shp = t->sobol_shift + (int64_t)rl * t->dim;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool aligned = (base & 127u) == 0u;
+    const uint64_t bidx = GRAY ? (base ^ (base >> 1)) : base;
+    for (int dd = warp; dd < Dc; dd += WARPS) {
+      const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
       if (aligned) {
-        x = S.xhi[dd] ^ S.lowtab[dd][idx & 127u];
+        uint32_t hi = sobol_word<false>(vd, shp[d0 + dd], (bidx >> 7) << 7);
+        uint32_t vk[7];
+#pragma unroll
+        for (int k = 0; k < 7; k++) vk[k] = vd[k];
+#pragma unroll
+        for (int m = 0; m < TILE / 32; m++) {
+          const uint32_t tt = (uint32_t)(lane + 32 * m);
+          const uint32_t i = (uint32_t)base + tt;
+          const uint32_t g = (GRAY ? (i ^ (i >> 1)) : i) & 127u;
+          uint32_t x = hi;
+#pragma unroll
+          for (int k = 0; k < 7; k++) x ^= (g >> k) & 1u ? vk[k] : 0u;
+          zt[dd * TILE + tt] = (double)x * TWO_M32;
+        }
       } else {
-        const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
-        x = shift[d0 + dd];
-        for (uint32_t bits = idx; bits; bits &= bits - 1u) x ^= vd[__ffs(bits) - 1];
+        for (int tt = lane; tt < TILE; tt += 32)
+          zt[dd * TILE + tt] =
+              (double)sobol_word<GRAY>(vd, shp[d0 + dd], base + (uint64_t)tt) * TWO_M32;
       }
-      zcol[dd * TILE] = (double)x * 2.3283064365386963e-10;
     }
   }
 };
 
 // SFC64 per-path stream (no reference counterpart; numpy SFC64 core):
 // state from derive_words(derive_key(seed, 7, m, path), 6), 12 warm-up
-// draws, u = (w >> 11) 2^-53 as numpy Generator.random().
+// draws, u = (w >> 11) 2^-53 as numpy Generator.random().  Dims are drawn
+// in order, so the state carries over between a path's chunks.
 struct GenSfc64 {
+  const RepTables *t;
   Sfc64 s;
-  __device__ void begin(const RepTables &t, int rl, uint64_t, uint64_t path, GenShared &,
-                        uint16_t *, int) {
-    uint64_t km = derive_key3(t.seed, 7, (uint64_t)(t.rep_first + rl));
-    sfc_seed(s, splitmix64(km ^ path));
-  }
-  __device__ void fill(int d0, int Dc, double *zt) {
+  using Shared = NoShared;
+  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
+    if (d0 == 0) {
+      uint64_t km = derive_key3(t->seed, 7, (uint64_t)(t->rep_first + rl));
+      sfc_seed(s, splitmix64(km ^ path));
+    }
     for (int dd = 0; dd < Dc; dd++)
-      zt[dd * TILE + threadIdx.x] = (double)(sfc_next(s) >> 11) * (1.0 / 9007199254740992.0);
+      zt[dd * TILE + threadIdx.x] = (double)(sfc_next(s) >> 11) * TWO_M53;
   }
 };
 
 // ======================================================================
-// Warp-cooperative inverse normal over a chunk (tail compaction)
+// Warp-cooperative inverse normal over the thread's own column of a chunk.
+// Comparisons run on the integer pipe (IEEE order of non-negative doubles
+// == order of their bit patterns); four inputs are in flight per pass for
+// ILP; the ~9% tail inputs are queued and evaluated 32 at a time.
 // ======================================================================
+__device__ __forceinline__ double invn_fold_i(double p, bool *neg) {
+  const long long HALF = 0x3FE0000000000000LL;   // 0.5
+  const long long TINYB = 0x3CA0000000000000LL;  // 2^-53
+  *neg = __double_as_longlong(p) > HALF;
+  double pl = *neg ? 1.0 - p : p;  // exact for p > 1/2
+  return __double_as_longlong(pl) < TINYB ? InvNormal::TINY : pl;
+}
+__device__ __forceinline__ bool invn_is_tail(double pl) {
+  return __double_as_longlong(pl) < __double_as_longlong(InvNormal::PLOW);
+}
+
 __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc, uint16_t *q) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   int qn = 0;
-  for (int dd = 0; dd < Dc; dd++) {
-    const int slot = dd * TILE + threadIdx.x;
-    bool neg;
-    double pl = invn_fold(zt[slot], &neg);
-    bool tail = pl < InvNormal::PLOW;
-    unsigned b = __ballot_sync(0xffffffffu, tail);
-    if (tail) {
-      q[qn + __popc(b & lt)] = (uint16_t)slot;
-    } else {
-      double x = invn_central(pl);
-      zt[slot] = neg ? -x : x;
+  for (int d4 = 0; d4 < Dc; d4 += 4) {
+    double pl[4], x[4];
+    bool neg[4], tail[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int dd = d4 + k;
+      double p = dd < Dc ? zt[dd * TILE + threadIdx.x] : 0.5;
+      pl[k] = invn_fold_i(p, &neg[k]);
+      tail[k] = dd < Dc && invn_is_tail(pl[k]);
     }
-    qn += __popc(b);
+#pragma unroll
+    for (int k = 0; k < 4; k++) x[k] = invn_central(pl[k]);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int dd = d4 + k;
+      const int slot = dd * TILE + threadIdx.x;
+      unsigned b = __ballot_sync(0xffffffffu, tail[k]);
+      if (tail[k]) q[qn + __popc(b & lt)] = (uint16_t)slot;
+      else if (dd < Dc) zt[slot] = neg[k] ? -x[k] : x[k];
+      qn += __popc(b);
+    }
   }
   __syncwarp();
   for (int k = lane; k < qn; k += 32) {
-    int slot = q[k];
+    const int slot = q[k];
     bool neg;
-    double pl = invn_fold(zt[slot], &neg);
+    double pl = invn_fold_i(zt[slot], &neg);
     double x = invn_tail(pl);
     zt[slot] = neg ? -x : x;
   }
@@ -520,31 +501,44 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc, uint16_t *q
 }
 
 // ======================================================================
-// Models (phase 2): thread-per-path state in registers
+// Models: thread-per-path state in registers
 // ======================================================================
 
-// LIBOR market-model caplet, one-factor Euler (models.py:271-293).  S static:
-// forward rates live in registers; for S <= CHUNK the whole triangle is
-// unrolled, above that the step loop is dynamic and the alive-rate loop is
-// unrolled with uniform guards.  Division by (1 + delta L) uses a MUFU seed
-// plus one Newton step in the drift (its weight in the path is ~1e-4, so
-// the ~2^-44 relative error is far below the 1e-12 parity bar) and two
-// steps everywhere else.
+// LIBOR market-model caplet, one-factor Euler (models.py:271-293).  The S
+// forward rates live in registers.  For S <= CHUNK the whole step/rate
+// triangle is unrolled; above that the step loop is dynamic and the rate
+// loop unrolled with uniform guards.  1/(1 + delta L) in the drift uses a
+// MUFU seed plus one Newton step (the drift's weight in the path is ~1e-4,
+// so the ~2^-44 relative error is far below the 1e-12 parity bar).  The
+// deflator prod (1 + delta L_i(T_i)) is formed as a product and inverted
+// once (each L_i is frozen after step i, so its final value is its fixing,
+// models.py:289-290).
 template <int S>
 struct ModelLibor {
   static constexpr bool NORMALS = true;
-  static constexpr int DIM = S;
+  static constexpr int MINB = S <= 20 ? 4 : (S <= 40 ? 3 : 2);  // CTAs/SM (register budget)
+  struct Shared {
+    double l0[S];
+  };
+  static __host__ __device__ int gen_dims(int dim) { return dim; }
+  const Shared *sh;
   double L[S];
-  double delta, s2d, ssq, g0;
-  __device__ void begin(const ModelParams &mp, const double *l0s) {
+  double delta, s2d, ssq, strike, ff;
+  __device__ void init(const ModelParams &mp_, Shared &s) {
+    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.table[n];
+    sh = &s;
+    strike = mp_.strike;
+    ff = mp_.front_factor;
+    delta = mp_.delta;
+    s2d = mp_.sigma * mp_.sigma * mp_.delta;
+    ssq = mp_.sigma * sqrt(mp_.delta);
+  }
+  __device__ void begin() {
 #pragma unroll
-    for (int n = 0; n < S; n++) L[n] = l0s[n];
-    delta = mp.delta;
-    s2d = mp.sigma * mp.sigma * mp.delta;
-    ssq = mp.sigma * sqrt(mp.delta);
+    for (int n = 0; n < S; n++) L[n] = sh->l0[n];
   }
   __device__ __forceinline__ void step(int i, double z) {
-    const double g1 = 1.0 + ssq * z;
+    const double g1 = fma(ssq, z, 1.0);
     double drift = 0.0;
 #pragma unroll
     for (int n = 0; n < S; n++) {
@@ -555,55 +549,85 @@ struct ModelLibor {
       }
     }
   }
-  __device__ void chunk(int d0, int Dc, const double *zcol, int stride) {
+  __device__ void chunk(int d0, int Dc, const double *zcol) {
     if (S <= CHUNK) {
 #pragma unroll
-      for (int i = 0; i < S; i++) step(i, zcol[i * stride]);
+      for (int i = 0; i < S; i++) step(i, zcol[i * TILE]);
     } else {
-      for (int k = 0; k < Dc; k++) step(d0 + k, zcol[k * stride]);
+      for (int k = 0; k < Dc; k++) step(d0 + k, zcol[k * TILE]);
     }
   }
-  __device__ double payoff(const ModelParams &mp) const {
-    // disc = front_factor / prod_{i<S-1} (1 + delta L_i(T_i)); L_i is frozen
-    // after step i, so its final value is the fixing (models.py:289-290).
-    double disc = mp.front_factor;
+  __device__ double payoff() const {
+    double prod = 1.0;
 #pragma unroll
-    for (int n = 0; n < S - 1; n++) disc *= rcp2(fma(delta, L[n], 1.0));
-    double lt = L[S - 1];
-    double pay = delta * fmax(lt - mp.strike, 0.0) * rcp2(fma(delta, lt, 1.0));
-    return pay * disc;
+    for (int n = 0; n < S - 1; n++) prod *= fma(delta, L[n], 1.0);
+    const double lt = L[S - 1];
+    const double pay = delta * fmax(lt - strike, 0.0);
+    return pay * ff * rcp2(fma(delta, lt, 1.0) * prod);
   }
 };
 
-// MBS present value (models.py:430-449), 360 monthly steps.
+// MBS present value (models.py:430-449), monthly steps.
 struct ModelMbs {
   static constexpr bool NORMALS = true;
-  double disc, rem, rate, prev_w, pv;
+  static constexpr int MINB = 4;
+  static constexpr int MAXM = 1 << 20;
+  using Shared = NoShared;
+  static __host__ __device__ int gen_dims(int dim) { return dim; }
   const double *ck;
-  __device__ void begin(const ModelParams &mp, const double *cks) {
+  double i0, sxi, k0, k1, k2, k3, k4, pay;
+  double disc, rem, rate, prev_w, pv;
+  __device__ void init(const ModelParams &mp_, Shared &) {
+    ck = mp_.table;  // annuity ratios: uniform across the warp, L1-resident
+    i0 = mp_.i0;
+    sxi = mp_.sigma_xi;
+    k0 = mp_.k0;
+    k1 = mp_.k1;
+    k2 = mp_.k2;
+    k3 = mp_.k3;
+    k4 = mp_.k4;
+    pay = mp_.payment;
+  }
+  __device__ void begin() {
     disc = 1.0;
     rem = 1.0;
-    rate = mp.i0;
+    rate = i0;
     prev_w = 0.0;
     pv = 0.0;
-    ck = cks;
   }
-  __device__ void chunk(int d0, int Dc, const double *zcol, int stride, const ModelParams &mp) {
+  __device__ void chunk(int d0, int Dc, const double *zcol) {
     for (int kk = 0; kk < Dc; kk++) {
       const int k = d0 + kk;  // month k+1
       disc *= rcp2(1.0 + rate);
       if (k > 0) rem *= 1.0 - prev_w;
-      double xi = mp.sigma_xi * zcol[kk * stride];
-      rate = mp.k0 * exp(xi) * rate;
-      double w = fma(mp.k2, atan(fma(mp.k3, rate, mp.k4)), mp.k1);
-      pv = fma(disc * mp.payment * rem, fma(w, ck[k], 1.0 - w), pv);
+      double xi = sxi * zcol[kk * TILE];
+      rate = k0 * exp(xi) * rate;
+      double w = fma(k2, atan(fma(k3, rate, k4)), k1);
+      pv = fma(disc * pay * rem, fma(w, __ldg(ck + k), 1.0 - w), pv);
       prev_w = w;
     }
   }
+  __device__ double payoff() const { return pv; }
+};
+
+// f = x_1 (FirstCoordinateModel, models.py:489-498) and f = 1 (ConstantModel).
+template <bool CONST1>
+struct ModelTest {
+  static constexpr bool NORMALS = false;
+  static constexpr int MINB = 4;
+  using Shared = NoShared;
+  static __host__ __device__ int gen_dims(int) { return CONST1 ? 0 : 1; }
+  double f;
+  __device__ void init(const ModelParams &, Shared &) {}
+  __device__ void begin() { f = 1.0; }
+  __device__ void chunk(int, int Dc, const double *zcol) {
+    if (!CONST1 && Dc > 0) f = zcol[0];
+  }
+  __device__ double payoff() const { return f; }
 };
 
 // ======================================================================
-// Fused path kernel
+// Fused, software-pipelined path kernel
 // ======================================================================
 struct PathArgs {
   RepTables t;
@@ -612,99 +636,62 @@ struct PathArgs {
   int64_t nmax;
   int64_t tiles_per_rep;
   double *payoffs;  // [rep_n][nmax]
-  int sig_cap;      // u16 sigma entries staged per chunk (0: read from global)
 };
 
-// dynamic shared memory: [model table doubles][staged sigma u16]
-__device__ __forceinline__ uint16_t *dyn_sig(void *dyn, int table_doubles) {
-  return reinterpret_cast<uint16_t *>(reinterpret_cast<double *>(dyn) + table_doubles);
-}
+constexpr size_t ZT_BYTES = sizeof(double) * CHUNK * TILE;  // one uniform/normal tile
 
-template <class G, int S>
-__global__ void __launch_bounds__(TILE) k_paths_libor(PathArgs a) {
-  __shared__ double zt[CHUNK * TILE];
+template <class G, class Mdl>
+__global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
+  extern __shared__ __align__(16) double zdyn[];  // 2 x ZT_BYTES (double buffer)
+  auto zbuf = [&](int64_t u) { return zdyn + (u & 1) * (CHUNK * TILE); };
   __shared__ uint16_t tq[WARPS][CHUNK * 32];
-  __shared__ GenShared gsh;
-  __shared__ double l0s[S];
-  extern __shared__ double dyn[];
-  uint16_t *sig_dyn = dyn_sig(dyn, 0);
-  for (int n = threadIdx.x; n < S; n += TILE) l0s[n] = a.mp.table[n];
+  __shared__ typename G::Shared gsh;
+  __shared__ typename Mdl::Shared msh;
+  Mdl md;
+  md.init(a.mp, msh);
+  G g;
+  g.setup(a.t, gsh);
   __syncthreads();
   const int warp = threadIdx.x >> 5;
+  const int gdims = Mdl::gen_dims(a.mp.dim);
+  const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
   const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
-  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-    const int rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
-    const int64_t base = (w % a.tiles_per_rep) * TILE;
-    const int64_t path = base + threadIdx.x;
-    G g;
-    g.begin(a.t, rl, (uint64_t)base, (uint64_t)path, gsh, sig_dyn, a.sig_cap);
-    ModelLibor<S> md;
-    md.begin(a.mp, l0s);
-    for (int d0 = 0; d0 < S; d0 += CHUNK) {
-      const int Dc = S - d0 < CHUNK ? S - d0 : CHUNK;
-      g.fill(d0, Dc, zt);
-      __syncwarp();
-      chunk_to_normals(zt, Dc, tq[warp]);
-      md.chunk(d0, Dc, zt + threadIdx.x, TILE);
-      __syncwarp();
-    }
-    if (path < a.nmax)
-      a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.payoff(a.mp);
-  }
-}
-
-template <class G>
-__global__ void __launch_bounds__(TILE) k_paths_mbs(PathArgs a) {
-  __shared__ double zt[CHUNK * TILE];
-  __shared__ uint16_t tq[WARPS][CHUNK * 32];
-  __shared__ GenShared gsh;
-  extern __shared__ double dyn[];
-  double *cks = dyn;
-  uint16_t *sig_dyn = dyn_sig(dyn, a.mp.dim);
-  for (int n = threadIdx.x; n < a.mp.dim; n += TILE) cks[n] = a.mp.table[n];
+  if ((int64_t)blockIdx.x >= total) return;
+  const int64_t ntile = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t nunit = ntile * nchunk;
+  // unit u -> (replication, tile base, chunk)
+  auto info = [&](int64_t u, int &rl, int64_t &base, int &d0, int &Dc) {
+    const int64_t k = u / nchunk;
+    const int c = (int)(u - k * nchunk);
+    const int64_t w = blockIdx.x + k * gridDim.x;
+    rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
+    base = (w % a.tiles_per_rep) * TILE;
+    d0 = c * CHUNK;
+    Dc = gdims - d0 < CHUNK ? gdims - d0 : CHUNK;
+  };
+  int rl, d0, Dc;
+  int64_t base;
+  info(0, rl, base, d0, Dc);
+  if (gdims > 0) g.unit(rl, (uint64_t)base, (uint64_t)(base + threadIdx.x), d0, Dc, zbuf(0));
   __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
-  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-    const int rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
-    const int64_t base = (w % a.tiles_per_rep) * TILE;
-    const int64_t path = base + threadIdx.x;
-    G g;
-    g.begin(a.t, rl, (uint64_t)base, (uint64_t)path, gsh, sig_dyn, a.sig_cap);
-    ModelMbs md;
-    md.begin(a.mp, cks);
-    for (int d0 = 0; d0 < a.mp.dim; d0 += CHUNK) {
-      const int Dc = a.mp.dim - d0 < CHUNK ? a.mp.dim - d0 : CHUNK;
-      g.fill(d0, Dc, zt);
-      __syncwarp();
-      chunk_to_normals(zt, Dc, tq[warp]);
-      md.chunk(d0, Dc, zt + threadIdx.x, TILE, a.mp);
-      __syncwarp();
+  for (int64_t u = 0; u < nunit; u++) {
+    info(u, rl, base, d0, Dc);
+    if (gdims > 0 && u + 1 < nunit) {  // generate the next unit into the other buffer
+      int rl1, d01, Dc1;
+      int64_t base1;
+      info(u + 1, rl1, base1, d01, Dc1);
+      g.unit(rl1, (uint64_t)base1, (uint64_t)(base1 + threadIdx.x), d01, Dc1, zbuf(u + 1));
     }
-    if (path < a.nmax) a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.pv;
-  }
-}
-
-// f = x_1 (FirstCoordinateModel, models.py:489-498) and f = 1 (ConstantModel).
-template <class G, bool CONST1>
-__global__ void __launch_bounds__(TILE) k_paths_test(PathArgs a) {
-  __shared__ double zt[TILE];
-  __shared__ GenShared gsh;
-  extern __shared__ double dyn[];
-  uint16_t *sig_dyn = dyn_sig(dyn, 0);
-  const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
-  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-    const int rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
-    const int64_t base = (w % a.tiles_per_rep) * TILE;
-    const int64_t path = base + threadIdx.x;
-    double f = 1.0;
-    if (!CONST1) {
-      G g;
-      g.begin(a.t, rl, (uint64_t)base, (uint64_t)path, gsh, sig_dyn, a.sig_cap);
-      g.fill(0, 1, zt);
-      f = zt[threadIdx.x];
+    double *z = zbuf(u);
+    if (d0 == 0) md.begin();
+    if (Mdl::NORMALS) chunk_to_normals(z, Dc, tq[warp]);
+    md.chunk(d0, Dc, z + threadIdx.x);
+    if (d0 + Dc >= gdims) {
+      const int64_t path = base + threadIdx.x;
+      if (path < a.nmax)
+        a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.payoff();
     }
-    if (path < a.nmax) a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = f;
+    __syncthreads();
   }
 }
 
@@ -715,20 +702,20 @@ __global__ void __launch_bounds__(TILE) k_paths_test(PathArgs a) {
 template <class G>
 __global__ void __launch_bounds__(TILE) k_points(RepTables t, int rl, int64_t first,
                                                  const int64_t *idx, int64_t count,
-                                                 double *out, int sig_cap) {
-  __shared__ double zt[CHUNK * TILE];
-  __shared__ GenShared gsh;
-  extern __shared__ double dyn[];
-  uint16_t *sig_dyn = dyn_sig(dyn, 0);
+                                                 double *out) {
+  extern __shared__ __align__(16) double zt[];  // ZT_BYTES
+  __shared__ typename G::Shared gsh;
+  G g;
+  g.setup(t, gsh);
   for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < count; tb += (int64_t)gridDim.x * TILE) {
     const int64_t r = tb + threadIdx.x;
     const bool ok = r < count;
     const int64_t path = idx ? (ok ? idx[r] : 0) : first + r;
-    G g;
-    g.begin(t, rl, (uint64_t)(first + tb), (uint64_t)path, gsh, sig_dyn, sig_cap);
     for (int d0 = 0; d0 < t.dim; d0 += CHUNK) {
       const int Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
-      g.fill(d0, Dc, zt);
+      __syncthreads();
+      g.unit(rl, (uint64_t)(first + tb), (uint64_t)path, d0, Dc, zt);
+      __syncthreads();
       if (ok)
         for (int dd = 0; dd < Dc; dd++) out[r * t.dim + d0 + dd] = zt[dd * TILE + threadIdx.x];
     }
@@ -736,31 +723,71 @@ __global__ void __launch_bounds__(TILE) k_points(RepTables t, int rl, int64_t fi
 }
 
 // ======================================================================
+// Stream throughput kernel (config 4): points [0, npoints) of dimension
+// t.dim, fused inverse normal, consumed by a sum (and optionally stored).
+// ======================================================================
+template <class G>
+__global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t npoints,
+                                                 double *block_sums, double *store) {
+  extern __shared__ __align__(16) double zt[];  // ZT_BYTES
+  __shared__ uint16_t tq[WARPS][CHUNK * 32];
+  __shared__ typename G::Shared gsh;
+  __shared__ double red[WARPS];
+  G g;
+  g.setup(t, gsh);
+  const int warp = threadIdx.x >> 5;
+  double acc = 0.0;
+  for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < npoints;
+       tb += (int64_t)gridDim.x * TILE) {
+    const int64_t r = tb + threadIdx.x;
+    const bool ok = r < npoints;
+    for (int d0 = 0; d0 < t.dim; d0 += CHUNK) {
+      const int Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
+      __syncthreads();
+      g.unit(rl, (uint64_t)tb, (uint64_t)r, d0, Dc, zt);
+      __syncthreads();
+      chunk_to_normals(zt, Dc, tq[warp]);
+      if (ok) {
+        for (int dd = 0; dd < Dc; dd++) {
+          double z = zt[dd * TILE + threadIdx.x];
+          acc += z;
+          if (store) store[r * t.dim + d0 + dd] = z;
+        }
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < WARPS; k++) s += red[k];
+    block_sums[blockIdx.x] = s;
+  }
+}
+
+// ======================================================================
 // Model payoffs from caller uniforms (model.payoffs(u), models.py:311-322,
 // 462-469): thread per path, scalar inverse normal.
 // ======================================================================
-template <int S>
-__global__ void k_libor_u(ModelParams mp, const double *u, int64_t npaths, double *out) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npaths) return;
-  ModelLibor<S> md;
-  md.begin(mp, mp.table);
-  for (int i = 0; i < S; i++) md.step(i, inv_normal(u[p * S + i]));
-  out[p] = md.payoff(mp);
-}
-
-__global__ void k_mbs_u(ModelParams mp, const double *u, int64_t npaths, double *out) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npaths) return;
-  ModelMbs md;
-  md.begin(mp, mp.table);
-  double z[CHUNK];
+template <class Mdl>
+__global__ void __launch_bounds__(TILE) k_payoffs_u(ModelParams mp, const double *u,
+                                                    int64_t npaths, double *out) {
+  __shared__ typename Mdl::Shared msh;
+  extern __shared__ __align__(16) double zt[];  // ZT_BYTES
+  Mdl md;
+  md.init(mp, msh);
+  __syncthreads();
+  int64_t p = (int64_t)blockIdx.x * TILE + threadIdx.x;
+  const bool ok = p < npaths;
+  md.begin();
   for (int d0 = 0; d0 < mp.dim; d0 += CHUNK) {
-    int Dc = mp.dim - d0 < CHUNK ? mp.dim - d0 : CHUNK;
-    for (int k = 0; k < Dc; k++) z[k] = inv_normal(u[p * mp.dim + d0 + k]);
-    md.chunk(d0, Dc, z, 1, mp);
+    const int Dc = mp.dim - d0 < CHUNK ? mp.dim - d0 : CHUNK;
+    for (int k = 0; k < Dc; k++)
+      zt[k * TILE + threadIdx.x] = ok ? inv_normal(u[p * mp.dim + d0 + k]) : 0.0;
+    md.chunk(d0, Dc, zt + threadIdx.x);
   }
-  out[p] = md.pv;
+  if (ok) out[p] = md.payoff();
 }
 
 __global__ void k_inv_normal(const double *u, int64_t n, double *out) {
@@ -825,51 +852,6 @@ __global__ void k_reduce(SumPlan plan, const double *pay, int64_t pay_stride, do
 }
 
 // ======================================================================
-// Stream throughput kernel (config 4): points [0, npoints) of dimension
-// t.dim, fused inverse normal, consumed by a sum (and optionally stored).
-// ======================================================================
-template <class G>
-__global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t npoints,
-                                                 double *block_sums, double *store, int sig_cap) {
-  __shared__ double zt[CHUNK * TILE];
-  __shared__ uint16_t tq[WARPS][CHUNK * 32];
-  __shared__ GenShared gsh;
-  __shared__ double red[WARPS];
-  extern __shared__ double dyn[];
-  uint16_t *sig_dyn = dyn_sig(dyn, 0);
-  const int warp = threadIdx.x >> 5;
-  double acc = 0.0;
-  for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < npoints; tb += (int64_t)gridDim.x * TILE) {
-    const int64_t r = tb + threadIdx.x;
-    const bool ok = r < npoints;
-    G g;
-    g.begin(t, rl, (uint64_t)tb, (uint64_t)r, gsh, sig_dyn, sig_cap);
-    for (int d0 = 0; d0 < t.dim; d0 += CHUNK) {
-      const int Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
-      g.fill(d0, Dc, zt);
-      __syncwarp();
-      chunk_to_normals(zt, Dc, tq[warp]);
-      if (ok) {
-        for (int dd = 0; dd < Dc; dd++) {
-          double z = zt[dd * TILE + threadIdx.x];
-          acc += z;
-          if (store) store[r * t.dim + d0 + dd] = z;
-        }
-      }
-      __syncwarp();
-    }
-  }
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[warp] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int k = 0; k < WARPS; k++) s += red[k];
-    block_sums[blockIdx.x] = s;
-  }
-}
-
-// ======================================================================
 // FP64 pipe peak probe: independent DFMA chains, no memory traffic.
 // ======================================================================
 constexpr int PEAK_CHAINS = 8;
@@ -890,11 +872,6 @@ __global__ void __launch_bounds__(256) k_dfma_peak(int iters, double seed, doubl
   if (s == 12345.678) sink[threadIdx.x] = s;  // keep the chains alive
 }
 
-cudaError_t launch_dfma_peak(int blocks, int iters, double *sink, cudaStream_t s) {
-  k_dfma_peak<<<blocks, 256, 0, s>>>(iters, 1.0, sink);
-  return cudaGetLastError();
-}
-
 // ======================================================================
 // Launchers
 // ======================================================================
@@ -909,13 +886,25 @@ static int sm_count() {
   return n;
 }
 
+// every kernel taking dynamic shared memory opts in to the full carve-out
 template <class K>
-static int persistent_blocks(K kernel, size_t dyn_smem, int64_t work) {
+static size_t prep_dyn(K kernel, size_t dyn) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  return dyn;
+}
+
+template <class K>
+static int persistent_blocks(K kernel, int64_t work, size_t dyn = 0) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TILE, dyn_smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TILE, dyn);
   if (per_sm < 1) per_sm = 1;
   int64_t b = (int64_t)per_sm * sm_count();
   return (int)(work < b ? (work < 1 ? 1 : work) : b);
+}
+
+cudaError_t launch_dfma_peak(int blocks, int iters, double *sink, cudaStream_t s) {
+  k_dfma_peak<<<blocks, 256, 0, s>>>(iters, 1.0, sink);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rasrap_setup(const RepTables &t, uint16_t *sigma, uint16_t *digits,
@@ -934,20 +923,13 @@ cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32
   return cudaGetLastError();
 }
 
-// sigma tables are read from global (L1-resident); no staging
-static int sig_cap_for(const RepTables &) { return 0; }
-static size_t dyn_bytes(int table_doubles, int sig_cap) {
-  return sizeof(double) * table_doubles + sizeof(uint16_t) * sig_cap;
-}
-
 template <class G>
 static cudaError_t points_t(const RepTables &t, int rl, int64_t first, const int64_t *idx,
                             int64_t count, double *out, cudaStream_t s) {
   int64_t tiles = (count + TILE - 1) / TILE;
-  int cap = idx ? 0 : sig_cap_for(t);
-  size_t dyn = dyn_bytes(0, cap);
-  int blocks = persistent_blocks(k_points<G>, dyn, tiles);
-  k_points<G><<<blocks, TILE, dyn, s>>>(t, rl, first, idx, count, out, cap);
+  size_t dyn = prep_dyn(k_points<G>, ZT_BYTES);
+  int blocks = persistent_blocks(k_points<G>, tiles, dyn);
+  k_points<G><<<blocks, TILE, dyn, s>>>(t, rl, first, idx, count, out);
   return cudaGetLastError();
 }
 
@@ -971,50 +953,38 @@ cudaError_t launch_points(const RepTables &t, int rl, int64_t first, const int64
   return cudaErrorInvalidValue;
 }
 
+template <class G, class Mdl>
+static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
+                            int *blocks_out) {
+  const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
+  size_t dyn = prep_dyn(k_paths<G, Mdl>, 2 * ZT_BYTES);
+  int blocks = persistent_blocks(k_paths<G, Mdl>, work, dyn);
+  if (blocks_out) *blocks_out = blocks;
+  if (probe) return cudaSuccess;
+  k_paths<G, Mdl><<<blocks, TILE, dyn, s>>>(a);
+  if (launched) *launched += 1;
+  return cudaGetLastError();
+}
+
 template <class G>
 static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
-                           int *blocks_out) {
-  const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
-  int blocks = 0;
+                           int *blocks) {
   switch (a.mp.kind) {
-    case MODEL_LIBOR: {
-      size_t dyn = dyn_bytes(0, a.sig_cap);
-#define RQ_LIBOR_CASE(SS)                                              \
-  case SS:                                                             \
-    blocks = persistent_blocks(k_paths_libor<G, SS>, dyn, work);       \
-    if (!probe) k_paths_libor<G, SS><<<blocks, TILE, dyn, s>>>(a);     \
-    break;
+    case MODEL_LIBOR:
       switch (a.mp.dim) {
-        RQ_LIBOR_CASE(10)
-        RQ_LIBOR_CASE(20)
-        RQ_LIBOR_CASE(40)
-        RQ_LIBOR_CASE(80)
-        default: return cudaErrorInvalidValue;
+        case 10: return paths_gm<G, ModelLibor<10>>(a, launched, s, probe, blocks);
+        case 20: return paths_gm<G, ModelLibor<20>>(a, launched, s, probe, blocks);
+        case 40: return paths_gm<G, ModelLibor<40>>(a, launched, s, probe, blocks);
+        case 80: return paths_gm<G, ModelLibor<80>>(a, launched, s, probe, blocks);
       }
-#undef RQ_LIBOR_CASE
-      break;
-    }
-    case MODEL_MBS: {
-      size_t dyn = dyn_bytes(a.mp.dim, a.sig_cap);
-      blocks = persistent_blocks(k_paths_mbs<G>, dyn, work);
-      if (!probe) k_paths_mbs<G><<<blocks, TILE, dyn, s>>>(a);
-      break;
-    }
-    case MODEL_X1: {
-      size_t dyn = dyn_bytes(0, a.sig_cap);
-      blocks = persistent_blocks(k_paths_test<G, false>, dyn, work);
-      if (!probe) k_paths_test<G, false><<<blocks, TILE, dyn, s>>>(a);
-      break;
-    }
-    case MODEL_CONST1:
-      blocks = persistent_blocks(k_paths_test<G, true>, 0, work);
-      if (!probe) k_paths_test<G, true><<<blocks, TILE, 0, s>>>(a);
-      break;
-    default: return cudaErrorInvalidValue;
+      return cudaErrorInvalidValue;
+    case MODEL_MBS:
+      if (a.mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
+      return paths_gm<G, ModelMbs>(a, launched, s, probe, blocks);
+    case MODEL_X1: return paths_gm<G, ModelTest<false>>(a, launched, s, probe, blocks);
+    case MODEL_CONST1: return paths_gm<G, ModelTest<true>>(a, launched, s, probe, blocks);
   }
-  if (blocks_out) *blocks_out = blocks;
-  if (launched && !probe) *launched += 1;
-  return probe ? cudaSuccess : cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 static cudaError_t paths_dispatch(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
@@ -1040,7 +1010,6 @@ cudaError_t launch_paths(const RepTables &t, const ModelParams &mp, int rep_loca
   a.nmax = nmax;
   a.tiles_per_rep = (nmax + TILE - 1) / TILE;
   a.payoffs = payoffs;
-  a.sig_cap = sig_cap_for(t);
   return paths_dispatch(a, launched, s, false, nullptr);
 }
 
@@ -1050,7 +1019,6 @@ int paths_grid_blocks(const RepTables &t, const ModelParams &mp) {
   a.mp = mp;
   a.rep_n = 1 << 20;
   a.tiles_per_rep = 1 << 20;
-  a.sig_cap = sig_cap_for(t);
   int blocks = 0;
   paths_dispatch(a, nullptr, 0, true, &blocks);
   return blocks;
@@ -1067,18 +1035,19 @@ cudaError_t launch_reduce(const SumPlan &plan, const double *payoffs, int64_t pa
 
 cudaError_t launch_model_payoffs(const ModelParams &mp, const double *u, int64_t npaths,
                                  double *out, cudaStream_t s) {
-  int blocks = (int)((npaths + 127) / 128);
+  int blocks = (int)((npaths + TILE - 1) / TILE);
   if (blocks < 1) return cudaSuccess;
   if (mp.kind == MODEL_MBS) {
-    k_mbs_u<<<blocks, 128, 0, s>>>(mp, u, npaths, out);
+    if (mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
+    k_payoffs_u<ModelMbs><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out);
     return cudaGetLastError();
   }
   if (mp.kind != MODEL_LIBOR) return cudaErrorInvalidValue;
   switch (mp.dim) {
-    case 10: k_libor_u<10><<<blocks, 128, 0, s>>>(mp, u, npaths, out); break;
-    case 20: k_libor_u<20><<<blocks, 128, 0, s>>>(mp, u, npaths, out); break;
-    case 40: k_libor_u<40><<<blocks, 128, 0, s>>>(mp, u, npaths, out); break;
-    case 80: k_libor_u<80><<<blocks, 128, 0, s>>>(mp, u, npaths, out); break;
+    case 10: k_payoffs_u<ModelLibor<10>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
+    case 20: k_payoffs_u<ModelLibor<20>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
+    case 40: k_payoffs_u<ModelLibor<40>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
+    case 80: k_payoffs_u<ModelLibor<80>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -1095,8 +1064,8 @@ cudaError_t launch_inv_normal(const double *u, int64_t n, double *out, cudaStrea
 template <class G>
 static cudaError_t stream_t(const RepTables &t, int rl, int64_t npoints, double *sums,
                             int nblocks, double *store, cudaStream_t s) {
-  int cap = sig_cap_for(t);
-  k_stream<G><<<nblocks, TILE, dyn_bytes(0, cap), s>>>(t, rl, npoints, sums, store, cap);
+  size_t dyn = prep_dyn(k_stream<G>, ZT_BYTES);
+  k_stream<G><<<nblocks, TILE, dyn, s>>>(t, rl, npoints, sums, store);
   return cudaGetLastError();
 }
 
@@ -1104,11 +1073,15 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
                                   double *block_sums, int nblocks, double *store,
                                   cudaStream_t s) {
   switch (t.gen) {
-    case GEN_RASRAP_RECURSIVE: return stream_t<GenRasrapRecTile>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_RASRAP_COUNTER: return stream_t<GenRasrapCounter>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_RASRAP_RECURSIVE:
+      return stream_t<GenRasrapRecTile>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_RASRAP_COUNTER:
+      return stream_t<GenRasrapCounter>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_PHILOX: return stream_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_SOBOL_GRAY: return stream_t<GenSobolTile<true>>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_SOBOL_COUNTER: return stream_t<GenSobolTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_SOBOL_GRAY:
+      return stream_t<GenSobolTile<true>>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_SOBOL_COUNTER:
+      return stream_t<GenSobolTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_SFC64: return stream_t<GenSfc64>(t, rl, npoints, block_sums, nblocks, store, s);
   }
   return cudaErrorInvalidValue;
