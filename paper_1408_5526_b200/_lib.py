@@ -11,10 +11,12 @@ ArithmeticError).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "librqmc_b200.so"
+# RQMC_B200_LIB: alternative build of the same ABI (A/B kernel experiments)
+LIB_PATH = Path(os.environ.get("RQMC_B200_LIB", HERE / "librqmc_b200.so"))
 
 RQ_OK, RQ_ERR_VALUE, RQ_ERR_CUDA, RQ_ERR_RANGE, RQ_ERR_NONFINITE = 0, -1, -2, -3, -4
 

@@ -26,6 +26,13 @@
 #include "rq_device.cuh"
 #include "rq_internal.h"
 
+#ifndef RQ_PIPELINE
+#define RQ_PIPELINE 0  // 1: generate unit u+1 while modelling unit u (double-buffered tile)
+#endif
+#ifndef RQ_MINB_SMALL
+#define RQ_MINB_SMALL 4  // CTAs per SM targeted for LIBOR S <= 20 (register budget)
+#endif
+
 namespace rq {
 
 constexpr int TILE = 128;          // paths per CTA tile = threads per CTA
@@ -243,6 +250,7 @@ struct GenRasrapRecTile {
     const uint64_t n0 = t->start[(int64_t)rl * t->dim + d];
     uint64_t qb = n0 + base, qn = n0;
     int j = 0, hB = -1;
+#pragma unroll 1
     while (qb != qn) {  // positions where B's prefix still differs from n0's
       uint64_t nb = div_base64(qb, h), nq = div_base64(qn, h);
       uint32_t db = (uint32_t)(qb - nb * p), dn = (uint32_t)(qn - nq * p);
@@ -254,6 +262,7 @@ struct GenRasrapRecTile {
     }
     int N = TILE, J = 0;
     R.nn[dd][0] = (int16_t)N;
+#pragma unroll 1
     while (N > 1) {
       uint32_t bj = J < j ? R.bd[dd][J] : n0d[J];
       if (J >= j) R.bd[dd][J] = (uint16_t)bj;
@@ -262,6 +271,7 @@ struct GenRasrapRecTile {
       R.nn[dd][J] = (int16_t)N;
     }
     double S = ini[hB + 1 > J ? hB + 1 : J];
+#pragma unroll 1
     for (int k = hB; k >= J; k--) S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
     R.J[dd] = J;
     R.hB[dd] = hB;
@@ -277,6 +287,7 @@ struct GenRasrapRecTile {
     __syncwarp();
     const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
     const double *gsum = t->sums + (int64_t)rl * t->sum_stride;
+#pragma unroll 1
     for (int dd = warp; dd < Dc; dd += WARPS) {
       const HaltonDim &h = c_hdim[d0 + dd];
       const uint32_t p = (uint32_t)h.base;
@@ -287,12 +298,14 @@ struct GenRasrapRecTile {
       double *prev = R.lev[warp][0], *next = R.lev[warp][1];
       if (lane == 0) prev[0] = R.sJ[dd];
       __syncwarp();
+#pragma unroll 1
       for (int j = J - 1; j >= 0; j--) {
         const int Nj = R.nn[dd][j];
         const uint32_t bj = R.bd[dd][j];
         const double wj = w[j], inij = ini[j];
         const bool at_n0 = j > hB;  // node 0 of this level has n0's prefix
         double *dst = j ? next : zt + dd * TILE;
+#pragma unroll 1
         for (int k = lane; k < Nj; k += 32) {
           const uint32_t x = bj + (uint32_t)k;
           const uint32_t par = div_base(x, h);
@@ -516,7 +529,7 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc, uint16_t *q
 template <int S>
 struct ModelLibor {
   static constexpr bool NORMALS = true;
-  static constexpr int MINB = S <= 20 ? 4 : (S <= 40 ? 3 : 2);  // CTAs/SM (register budget)
+  static constexpr int MINB = S <= 20 ? RQ_MINB_SMALL : (S <= 40 ? 3 : 2);  // CTAs/SM
   struct Shared {
     double l0[S];
   };
@@ -659,30 +672,43 @@ __global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
   if ((int64_t)blockIdx.x >= total) return;
   const int64_t ntile = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int64_t nunit = ntile * nchunk;
-  // unit u -> (replication, tile base, chunk)
-  auto info = [&](int64_t u, int &rl, int64_t &base, int &d0, int &Dc) {
-    const int64_t k = u / nchunk;
-    const int c = (int)(u - k * nchunk);
-    const int64_t w = blockIdx.x + k * gridDim.x;
-    rl = a.rep_local0 + (int)(w / a.tiles_per_rep);
-    base = (w % a.tiles_per_rep) * TILE;
-    d0 = c * CHUNK;
-    Dc = gdims - d0 < CHUNK ? gdims - d0 : CHUNK;
+  // unit cursor: (replication, tile base, chunk) advanced incrementally
+  struct Cursor {
+    int rl, c;
+    int64_t base;
   };
-  int rl, d0, Dc;
-  int64_t base;
-  info(0, rl, base, d0, Dc);
-  if (gdims > 0) g.unit(rl, (uint64_t)base, (uint64_t)(base + threadIdx.x), d0, Dc, zbuf(0));
+  const int64_t rep_span = a.tiles_per_rep * TILE;
+  const int64_t stride = (int64_t)gridDim.x * TILE;
+  auto advance = [&](Cursor &q) {
+    if (++q.c == nchunk) {
+      q.c = 0;
+      q.base += stride;
+      while (q.base >= rep_span) {
+        q.base -= rep_span;
+        q.rl++;
+      }
+    }
+  };
+  Cursor cur{a.rep_local0 + (int)(blockIdx.x / a.tiles_per_rep), 0,
+             (int64_t)(blockIdx.x % a.tiles_per_rep) * TILE};
+  auto dc_of = [&](int c) { return gdims - c * CHUNK < CHUNK ? gdims - c * CHUNK : CHUNK; };
+  if (RQ_PIPELINE && gdims > 0)
+    g.unit(cur.rl, (uint64_t)cur.base, (uint64_t)(cur.base + threadIdx.x), 0, dc_of(0), zbuf(0));
   __syncthreads();
   for (int64_t u = 0; u < nunit; u++) {
-    info(u, rl, base, d0, Dc);
-    if (gdims > 0 && u + 1 < nunit) {  // generate the next unit into the other buffer
-      int rl1, d01, Dc1;
-      int64_t base1;
-      info(u + 1, rl1, base1, d01, Dc1);
-      g.unit(rl1, (uint64_t)base1, (uint64_t)(base1 + threadIdx.x), d01, Dc1, zbuf(u + 1));
+    Cursor nxt = cur;
+    advance(nxt);
+    const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
+    const int64_t base = cur.base;
+    double *z = zbuf(RQ_PIPELINE ? u : 0);
+    if (RQ_PIPELINE) {
+      if (gdims > 0 && u + 1 < nunit)  // generate the next unit into the other buffer
+        g.unit(nxt.rl, (uint64_t)nxt.base, (uint64_t)(nxt.base + threadIdx.x), nxt.c * CHUNK,
+               dc_of(nxt.c), zbuf(u + 1));
+    } else if (gdims > 0) {
+      g.unit(rl, (uint64_t)base, (uint64_t)(base + threadIdx.x), d0, Dc, z);
+      __syncthreads();
     }
-    double *z = zbuf(u);
     if (d0 == 0) md.begin();
     if (Mdl::NORMALS) chunk_to_normals(z, Dc, tq[warp]);
     md.chunk(d0, Dc, z + threadIdx.x);
@@ -692,6 +718,7 @@ __global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
         a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.payoff();
     }
     __syncthreads();
+    cur = nxt;
   }
 }
 
@@ -957,7 +984,7 @@ template <class G, class Mdl>
 static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                             int *blocks_out) {
   const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
-  size_t dyn = prep_dyn(k_paths<G, Mdl>, 2 * ZT_BYTES);
+  size_t dyn = prep_dyn(k_paths<G, Mdl>, (RQ_PIPELINE ? 2 : 1) * ZT_BYTES);
   int blocks = persistent_blocks(k_paths<G, Mdl>, work, dyn);
   if (blocks_out) *blocks_out = blocks;
   if (probe) return cudaSuccess;
