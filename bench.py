@@ -152,6 +152,9 @@ def run_ours(args) -> dict:
         torch.cuda.set_device(0)
     lib = _lib.lib()
     kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
+    if args.reps:
+        M = args.reps
+        desc += f" [M overridden to {M} per GPU]"
     model = build_model(kind, mat, acc)
     gen = args.generator
     gen_id = _lib.GEN_IDS[gen]
@@ -348,6 +351,8 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--generator", default="rasrap-recursive")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reps", type=int, default=0,
+                    help="override M (replications per GPU) for quick sub-runs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

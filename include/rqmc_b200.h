@@ -136,6 +136,9 @@ int rq_fp64_peak(double *slots_per_s, double *ms);
 /* Host-side constant tables (for tests and the Python shim). */
 int rq_sobol_directions(int dim, uint32_t *v_host); /* default_table(dim).v sobol.py:170 */
 int rq_halton_constants(int dim, int32_t *base, int32_t *K, double *scale0);
+/* The device's division-by-base magic for dimension d, evaluated on the
+ * host: q64 = floor(x / p) for x < 2^46, q32 = floor((uint32)x / p). */
+int rq_halton_divide(int d, uint64_t x, uint64_t *q64, uint32_t *q32);
 
 #ifdef __cplusplus
 }

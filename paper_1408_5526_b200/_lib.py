@@ -87,11 +87,12 @@ def _declare(L):
     L.rq_fp64_peak.argtypes = [P(dbl), P(dbl)]
     L.rq_sobol_directions.argtypes = [C.c_int, P(C.c_uint32)]
     L.rq_halton_constants.argtypes = [C.c_int, P(C.c_int32), P(C.c_int32), P(dbl)]
+    L.rq_halton_divide.argtypes = [C.c_int, u64, P(u64), P(C.c_uint32)]
     for name in ("rq_sampler_create", "rq_sampler_points", "rq_sampler_points_at",
                  "rq_sampler_rasrap_tables", "rq_estimate", "rq_run_replications",
                  "rq_model_payoffs", "rq_inv_normal", "rq_stream_normals", "rq_pairwise_sum",
                  "rq_pairwise_sum_host", "rq_fp64_peak",
-                 "rq_sobol_directions", "rq_halton_constants"):
+                 "rq_sobol_directions", "rq_halton_constants", "rq_halton_divide"):
         getattr(L, name).restype = C.c_int
 
 

@@ -319,6 +319,17 @@ int rq_abi_version(void) { return RQ_ABI_VERSION; }
 
 int rq_sobol_directions(int dim, uint32_t *v_host) { return sobol_v(dim, v_host); }
 
+int rq_halton_divide(int d, uint64_t x, uint64_t *q64, uint32_t *q32) {
+  if (d < 0 || d >= rq::MAX_DIM) return fail(RQ_ERR_VALUE, "dim index %d outside 0..%d", d, rq::MAX_DIM - 1);
+  const rq::HaltonDim &h = host_tables().dims[d];
+  if (q64) *q64 = rq::umulhi64(x, h.m64);
+  if (q32) {
+    uint32_t t = (uint32_t)x;
+    *q32 = (uint32_t)((((uint64_t)rq::umulhi32(t, h.mlo)) + t) >> h.ell);
+  }
+  return RQ_OK;
+}
+
 int rq_halton_constants(int dim, int32_t *base, int32_t *K, double *scale0) {
   if (dim < 1 || dim > rq::MAX_DIM) return fail(RQ_ERR_VALUE, "dim %d outside 1..%d", dim, rq::MAX_DIM);
   const HostTables &T = host_tables();
