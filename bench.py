@@ -48,7 +48,10 @@ WORKLOADS = {
     "c2": ("libor", 5.0, 0.25, 1024, 2**20, "C2 LIBOR caplet S=20 (T=5, delta=0.25), M=1024 x N=2^20"),
     "c3": ("mbs", None, None, 256, 10**6, "C3 MBS 360 months, M=256 x N=10^6"),
     "c5": ("libor", 20.0, 0.25, 8192, 2**20, "C5 LIBOR caplet S=80 (T=20, delta=0.25), M=8192 x N=2^20"),
+    "c4": ("stream", None, None, 1, 27_777_778,
+           "C4 stream: 360-dim points with fused inverse normal, 10^10 normals per step"),
 }
+NORMAL_SLOTS = 36  # Phi^-1 per normal
 
 
 def build_model(kind, maturity, accrual):
@@ -130,6 +133,63 @@ def device_step(gen_id, model, seed, first, count, grid, theta, lib, C, _lib):
     _lib.check(lib.rq_estimate(h, C.byref(ms), g.ctypes.data_as(C.POINTER(C.c_int64)), g.size,
                                theta.data_ptr(), C.byref(n), st))
     return h, n.value + (1 if gen_id in (0, 1, 3, 4) else 0), keep
+
+
+def run_stream(args) -> dict:
+    """Config 4: 10^10 normals of one generator (s = 360 points, Phi^-1 fused,
+    consumed by a sum) per step."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_1408_5526_b200 import _lib
+
+    torch.cuda.set_device(0)
+    lib = _lib.lib()
+    dim, npts = 360, WORKLOADS["c4"][4]
+    if args.reps:
+        npts = args.reps
+    h = C.c_void_p()
+    st = _lib.stream_ptr()
+    _lib.check(lib.rq_sampler_create(C.byref(h), _lib.GEN_IDS[args.generator], dim, SEED, 0, 1,
+                                     st))
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    peak, _ = _lib.fp64_peak()
+
+    def step():
+        _lib.check(lib.rq_stream_normals(h, 0, npts, out.data_ptr(), None, st))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    ms = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        step()
+        b.record()
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    clk = clocks.stop()
+    lib.rq_sampler_destroy(h)
+    t = float(np.mean(ms))
+    normals = npts * dim
+    value = normals / (t * 1e-3)
+    return {
+        "metric": "C4 normals/sec (fused inverse normal, s=360 stream)", "value": value,
+        "unit": "normals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seed 20120224, replication 0)",
+        "config": {"workload": WORKLOADS["c4"][5], "generator": args.generator,
+                   "points": npts, "dim": dim, "sum_check": float(out.item())},
+        "roofline": {"bound": "fp64", "achieved": value * NORMAL_SLOTS / 1e12,
+                     "peak": peak / 1e12, "unit": "Tslot/s (36 slots/normal)",
+                     "frac": value * NORMAL_SLOTS / peak},
+        "clocks": clk,
+    }
 
 
 def run_ours(args) -> dict:
@@ -356,7 +416,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.workload == "c4" and args.impl == "ours":
+        out = run_stream(args)
+    else:
+        out = run_reference(args) if args.impl == "reference" else run_ours(args)
     if out is not None:
         print(json.dumps(out))
 

@@ -305,7 +305,7 @@ struct GenRasrapRecTile {
         const double wj = w[j], inij = ini[j];
         const bool at_n0 = j > hB;  // node 0 of this level has n0's prefix
         double *dst = j ? next : zt + dd * TILE;
-#pragma unroll 1
+#pragma unroll 2
         for (int k = lane; k < Nj; k += 32) {
           const uint32_t x = bj + (uint32_t)k;
           const uint32_t par = div_base(x, h);
@@ -421,7 +421,7 @@ struct GenSobolTile {
         uint32_t vk[7];
 #pragma unroll
         for (int k = 0; k < 7; k++) vk[k] = vd[k];
-#pragma unroll
+#pragma unroll 2
         for (int m = 0; m < TILE / 32; m++) {
           const uint32_t tt = (uint32_t)(lane + 32 * m);
           const uint32_t i = (uint32_t)base + tt;
@@ -684,17 +684,49 @@ struct ModelMbs {
     prev_w = 0.0;
     pv = 0.0;
   }
+  __device__ __forceinline__ void month(int k, double xi) {  // month k+1
+    disc *= rcp2(1.0 + rate);
+    if (k > 0) rem *= 1.0 - prev_w;
+    rate = k0 * exp_mbs(xi) * rate;
+    double w = fma(k2, atan_mbs(fma(k3, rate, k4)), k1);
+    pv = fma(disc * pay * rem, fma(w, __ldg(ck + k), 1.0 - w), pv);
+    prev_w = w;
+  }
+  // Months in groups of MG: the shocks' exponentials, the discount
+  // reciprocals and the prepayment arctangents of a group are independent
+  // once the (cheap, serial) rate product is known, so they are issued
+  // together; only disc / rem / pv remain serial.  Same operations and
+  // association as month() (models.py:437-448).
+  static constexpr int MG = 4;
   __device__ void chunk(int d0, int Dc, const double *zcol) {
-    for (int kk = 0; kk < Dc; kk++) {
-      const int k = d0 + kk;  // month k+1
-      disc *= rcp2(1.0 + rate);
-      if (k > 0) rem *= 1.0 - prev_w;
-      double xi = sxi * zcol[kk * TILE];
-      rate = k0 * exp_mbs(xi) * rate;
-      double w = fma(k2, atan_mbs(fma(k3, rate, k4)), k1);
-      pv = fma(disc * pay * rem, fma(w, __ldg(ck + k), 1.0 - w), pv);
-      prev_w = w;
+    int kk = 0;
+    for (; kk + MG <= Dc; kk += MG) {
+      double e[MG], inv[MG], w[MG];
+#pragma unroll
+      for (int m = 0; m < MG; m++) e[m] = k0 * exp_mbs(sxi * zcol[(kk + m) * TILE]);
+      double r = rate;
+#pragma unroll
+      for (int m = 0; m < MG; m++) {
+        inv[m] = 1.0 + r;  // u_k uses the rate before this month's update
+        r = e[m] * r;
+        w[m] = r;
+      }
+#pragma unroll
+      for (int m = 0; m < MG; m++) {
+        inv[m] = rcp2(inv[m]);
+        w[m] = fma(k2, atan_mbs(fma(k3, w[m], k4)), k1);
+      }
+#pragma unroll
+      for (int m = 0; m < MG; m++) {
+        const int k = d0 + kk + m;
+        disc *= inv[m];
+        if (k > 0) rem *= 1.0 - prev_w;
+        pv = fma(disc * pay * rem, fma(w[m], __ldg(ck + k), 1.0 - w[m]), pv);
+        prev_w = w[m];
+      }
+      rate = r;
     }
+    for (; kk < Dc; kk++) month(d0 + kk, sxi * zcol[kk * TILE]);
   }
   __device__ double payoff() const { return pv; }
 };
