@@ -131,6 +131,7 @@ const HostTables &host_tables() {
       // M = ceil(2^(46+ell)/p); stored pre-shifted so q = umulhi64(x, m64)
       unsigned __int128 M = ((((unsigned __int128)1) << (46 + ell)) + p - 1) / p;
       h.m64 = (uint64_t)(M << (18 - ell));
+      h.m16 = (uint32_t)(((((uint64_t)1) << 32) + p - 1) / p);  // ceil(2^32/p)
       h.sig_off = sig;
       h.dig_off = dig;
       h.sum_off = sum;
@@ -326,6 +327,7 @@ int rq_halton_divide(int d, uint64_t x, uint64_t *q64, uint32_t *q32) {
   if (q32) {
     uint32_t t = (uint32_t)x;
     *q32 = (uint32_t)((((uint64_t)rq::umulhi32(t, h.mlo)) + t) >> h.ell);
+    if (t < 65536u && rq::umulhi32(t, h.m16) != *q32) *q32 = 0xFFFFFFFFu;  // 16-bit magic check
   }
   return RQ_OK;
 }

@@ -154,6 +154,8 @@ __global__ void k_sobol_setup(RepTables t, const uint32_t *v, uint32_t *gen_v,
 // ======================================================================
 constexpr int LEVBUF = 80;  // nodes per level buffer (>= TILE/2 + 2)
 
+constexpr int SIGD_MAX = 1024;  // sigma entries staged as doubles (single-chunk dims)
+
 struct RasrapTileShared {
   uint16_t bd[CHUNK][MAX_CAP];     // base-p digits of the tile base B = n0 + base
   int16_t nn[CHUNK][MAX_CAP + 1];  // nodes per level: distinct prefixes floor(n / p^j)
@@ -161,6 +163,12 @@ struct RasrapTileShared {
   int32_t hB[CHUNK];               // highest digit where B differs from n0 (-1: B == n0)
   double sJ[CHUNK];                // stream partial sum S_J of the top node
   double lev[WARPS][2][LEVBUF];    // per-warp ping-pong level buffers
+  // persistent stream state (single-chunk models, consecutive tiles of a CTA)
+  double P[CHUNK][MAX_CAP + 1];    // S_j(B), j = 0..cap
+  int32_t st_rl[CHUNK];            // replication the state belongs to (-1: none)
+  uint64_t st_base[CHUNK];         // tile base the state belongs to
+  int32_t soff[CHUNK];             // offset of sigma_d in sigd
+  double sigd[SIGD_MAX];           // sigma of the replication's dims as doubles
 };
 struct RasrapDirectShared {
   uint16_t scr[MAX_CAP][TILE];  // per-thread digits (direct path)
@@ -204,7 +212,7 @@ struct GenRasrapRecDirect {
   using Shared = RasrapDirectShared;
   const RepTables *t;
   Shared *sh;
-  __device__ void setup(const RepTables &t_, Shared &s) {
+  __device__ void setup(const RepTables &t_, Shared &s, int = 0) {
     t = &t_;
     sh = &s;
   }
@@ -234,12 +242,18 @@ struct GenRasrapRecTile {
   using Shared = RasrapTileShared;
   const RepTables *t;
   Shared *sh;
-  __device__ void setup(const RepTables &t_, Shared &s) {
+  bool persist;   // consecutive tiles of one CTA share a persistent stream state
+  bool sig_smem;  // sigma of the dims staged in shared memory as doubles
+  __device__ void setup(const RepTables &t_, Shared &s, int gdims = 0) {
     t = &t_;
     sh = &s;
+    persist = gdims > 0 && gdims <= CHUNK;
+    sig_smem = persist && c_hdim[gdims - 1].sig_off + c_hdim[gdims - 1].base <= SIGD_MAX;
+    for (int k = threadIdx.x; k < CHUNK; k += TILE) s.st_rl[k] = -1;
   }
-  // per-dim tile state (one lane per dim): digits of B, hB, level sizes, S_J
-  __device__ void prepare_dim(int rl, uint64_t base, int d, int dd) {
+  // Full state at B = n0 + base: digits, hB, P[j] = S_j(B) (chain from
+  // init_sums[hB+1]); used for a CTA's first tile of a replication.
+  __device__ void state_full(int rl, uint64_t base, int d, int dd) {
     RasrapTileShared &R = *sh;
     const HaltonDim &h = c_hdim[d];
     const uint32_t p = (uint32_t)h.base;
@@ -260,26 +274,95 @@ struct GenRasrapRecTile {
       qn = nq;
       j++;
     }
+#pragma unroll 1
+    for (; j < h.cap; j++) R.bd[dd][j] = n0d[j];
+#pragma unroll 1
+    for (int k = h.cap; k > hB; k--) R.P[dd][k] = ini[k];
+    double S = ini[hB + 1];
+#pragma unroll 1
+    for (int k = hB; k >= 0; k--) {
+      S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
+      R.P[dd][k] = S;
+    }
+    R.hB[dd] = hB;
+  }
+  // Odometer step B -> B + TILE (the adding machine on the digit vector):
+  // add TILE's base-p digits with carry, then re-chain the partial sums
+  // below the highest changed digit.
+  __device__ void state_advance(int rl, int d, int dd) {
+    RasrapTileShared &R = *sh;
+    const HaltonDim &h = c_hdim[d];
+    const uint32_t p = (uint32_t)h.base;
+    const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
+    const double *w = g_wts + h.sum_off;
+    uint32_t r = TILE, carry = 0;
+    int j = 0, jmax = -1;
+#pragma unroll 1
+    while (r != 0u || carry != 0u) {
+      const uint32_t q = __umulhi(r, h.m16);
+      const uint32_t b = R.bd[dd][j];
+      uint32_t a = b + (r - q * p) + carry;
+      carry = a >= p;
+      a = carry ? a - p : a;
+      R.bd[dd][j] = (uint16_t)a;
+      jmax = a != b ? j : jmax;
+      r = q;
+      j++;
+    }
+    int hB = R.hB[dd];
+    hB = jmax > hB ? jmax : hB;  // a carry above hB makes that digit exceed n0's
+    R.hB[dd] = hB;
+    double S = R.P[dd][jmax + 1];
+    const double *sgd = R.sigd + R.soff[dd];
+    const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
+#pragma unroll 1
+    for (int k = jmax; k >= 0; k--) {
+      const double sv = sig_smem ? sgd[R.bd[dd][k]] : u16d(sg[R.bd[dd][k]]);
+      S = k > hB ? ini[k] : dadd(S, dmul(sv, w[k]));
+      R.P[dd][k] = S;
+    }
+  }
+  // per-dim tile state (one lane per dim): digits of B, hB, level sizes, S_J
+  __device__ void prepare_dim(int rl, uint64_t base, int d, int dd) {
+    RasrapTileShared &R = *sh;
+    const HaltonDim &h = c_hdim[d];
+    if (persist && R.st_rl[dd] == rl && R.st_base[dd] + TILE == base) {
+      state_advance(rl, d, dd);
+    } else {
+      state_full(rl, base, d, dd);
+    }
+    R.st_rl[dd] = rl;
+    R.st_base[dd] = base;
     int N = TILE, J = 0;
     R.nn[dd][0] = (int16_t)N;
 #pragma unroll 1
     while (N > 1) {
-      uint32_t bj = J < j ? R.bd[dd][J] : n0d[J];
-      if (J >= j) R.bd[dd][J] = (uint16_t)bj;
-      N = (int)div_base(bj + (uint32_t)N - 1u, h) + 1;
+      N = (int)__umulhi((uint32_t)R.bd[dd][J] + (uint32_t)N - 1u, h.m16) + 1;
       J++;
       R.nn[dd][J] = (int16_t)N;
     }
-    double S = ini[hB + 1 > J ? hB + 1 : J];
-#pragma unroll 1
-    for (int k = hB; k >= J; k--) S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
     R.J[dd] = J;
-    R.hB[dd] = hB;
-    R.sJ[dd] = S;
+    R.sJ[dd] = R.P[dd][J];
+  }
+  __device__ void stage_sigma(int rl, int d0, int Dc) {
+    // warp w stages the sigma tables of its dims (dd = w mod WARPS)
+    RasrapTileShared &R = *sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
+    const int off0 = c_hdim[d0].sig_off;
+#pragma unroll 1
+    for (int dd = warp; dd < Dc; dd += WARPS) {
+      const HaltonDim &h = c_hdim[d0 + dd];
+      const int o = h.sig_off - off0;
+      for (int a = lane; a < h.base; a += 32) R.sigd[o + a] = (double)gsig[h.sig_off + a];
+      if (lane == 0) R.soff[dd] = o;
+    }
+    __syncwarp();
   }
   __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
     RasrapTileShared &R = *sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (sig_smem && R.st_rl[warp < Dc ? warp : 0] != rl) stage_sigma(rl, d0, Dc);
     {  // lane k prepares dim dd = warp + k * WARPS
       const int dd = warp + lane * WARPS;
       if (dd < Dc) prepare_dim(rl, base, d0 + dd, dd);
@@ -290,8 +373,9 @@ struct GenRasrapRecTile {
 #pragma unroll 1
     for (int dd = warp; dd < Dc; dd += WARPS) {
       const HaltonDim &h = c_hdim[d0 + dd];
-      const uint32_t p = (uint32_t)h.base;
+      const uint32_t p = (uint32_t)h.base, m16 = h.m16;
       const uint16_t *sg = gsig + h.sig_off;
+      const double *sgd = R.sigd + R.soff[dd];
       const double *ini = gsum + h.sum_off;
       const double *w = g_wts + h.sum_off;
       const int J = R.J[dd], hB = R.hB[dd];
@@ -307,10 +391,11 @@ struct GenRasrapRecTile {
         double *dst = j ? next : zt + dd * TILE;
 #pragma unroll 2
         for (int k = lane; k < Nj; k += 32) {
-          const uint32_t x = bj + (uint32_t)k;
-          const uint32_t par = div_base(x, h);
+          const uint32_t x = bj + (uint32_t)k;  // < 2^16
+          const uint32_t par = __umulhi(x, m16);
           const uint32_t a = x - par * p;
-          double v = dadd(prev[par], dmul(u16d(sg[a]), wj));
+          const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
+          double v = dadd(prev[par], dmul(sv, wj));
           dst[k] = (at_n0 && k == 0) ? inij : v;
         }
         __syncwarp();
@@ -329,7 +414,7 @@ struct GenRasrapRecTile {
 struct GenRasrapCounter {
   const RepTables *t;
   using Shared = NoShared;
-  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void setup(const RepTables &t_, Shared &, int = 0) { t = &t_; }
   __device__ __forceinline__ double value(int rl, int d, uint32_t i) const {
     const HaltonDim &h = c_hdim[d];
     const uint16_t *d0 = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
@@ -358,7 +443,7 @@ struct GenRasrapCounter {
 struct GenPhilox {
   const RepTables *t;
   using Shared = NoShared;
-  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void setup(const RepTables &t_, Shared &, int = 0) { t = &t_; }
   __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
     const uint64_t key = derive_key3(t->seed, 3, (uint64_t)(t->rep_first + rl));
     const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
@@ -389,7 +474,7 @@ template <bool GRAY>
 struct GenSobolDirect {
   const RepTables *t;
   using Shared = NoShared;
-  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void setup(const RepTables &t_, Shared &, int = 0) { t = &t_; }
   __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
     const uint32_t *v = t->sobol_v + (int64_t)rl * t->dim * SOBOL_BITS;
     const uint32_t *sh = t->sobol_shift + (int64_t)rl * t->dim;
@@ -407,7 +492,7 @@ template <bool GRAY>
 struct GenSobolTile {
   const RepTables *t;
   using Shared = NoShared;
-  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void setup(const RepTables &t_, Shared &, int = 0) { t = &t_; }
   __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
     const uint32_t *v = t->sobol_v + (int64_t)rl * t->dim * SOBOL_BITS;
     const uint32_t *shp = t->sobol_shift + (int64_t)rl * t->dim;
@@ -448,7 +533,7 @@ struct GenSfc64 {
   const RepTables *t;
   Sfc64 s;
   using Shared = NoShared;
-  __device__ void setup(const RepTables &t_, Shared &) { t = &t_; }
+  __device__ void setup(const RepTables &t_, Shared &, int = 0) { t = &t_; }
   __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
     if (d0 == 0) {
       uint64_t km = derive_key3(t->seed, 7, (uint64_t)(t->rep_first + rl));
@@ -770,23 +855,26 @@ __global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
   __shared__ typename Mdl::Shared msh;
   Mdl md;
   md.init(a.mp, msh);
-  G g;
-  g.setup(a.t, gsh);
-  __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int gdims = Mdl::gen_dims(a.mp.dim);
+  G g;
+  g.setup(a.t, gsh, gdims);
+  __syncthreads();
   const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
   const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
   if ((int64_t)blockIdx.x >= total) return;
-  const int64_t ntile = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t nunit = ntile * nchunk;
+  // CTA b owns the contiguous tiles [lo, hi) of the batch (rep-major), so
+  // consecutive tiles of a replication stay on one CTA (persistent
+  // generator state, L1 locality of the replication's tables)
+  const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
+  const int64_t nunit = (hi - lo) * nchunk;
   // unit cursor: (replication, tile base, chunk) advanced incrementally
   struct Cursor {
     int rl, c;
     int64_t base;
   };
   const int64_t rep_span = a.tiles_per_rep * TILE;
-  const int64_t stride = (int64_t)gridDim.x * TILE;
+  const int64_t stride = TILE;
   auto advance = [&](Cursor &q) {
     if (++q.c == nchunk) {
       q.c = 0;
@@ -797,8 +885,8 @@ __global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
       }
     }
   };
-  Cursor cur{a.rep_local0 + (int)(blockIdx.x / a.tiles_per_rep), 0,
-             (int64_t)(blockIdx.x % a.tiles_per_rep) * TILE};
+  Cursor cur{a.rep_local0 + (int)(lo / a.tiles_per_rep), 0,
+             (int64_t)(lo % a.tiles_per_rep) * TILE};
   auto dc_of = [&](int c) { return gdims - c * CHUNK < CHUNK ? gdims - c * CHUNK : CHUNK; };
   if (RQ_PIPELINE && gdims > 0)
     g.unit(cur.rl, (uint64_t)cur.base, (uint64_t)(cur.base + threadIdx.x), 0, dc_of(0), zbuf(0));
@@ -841,7 +929,8 @@ __global__ void __launch_bounds__(TILE) k_points(RepTables t, int rl, int64_t fi
   extern __shared__ __align__(16) double zt[];  // ZT_BYTES
   __shared__ typename G::Shared gsh;
   G g;
-  g.setup(t, gsh);
+  g.setup(t, gsh, t.dim);
+  __syncthreads();
   for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < count; tb += (int64_t)gridDim.x * TILE) {
     const int64_t r = tb + threadIdx.x;
     const bool ok = r < count;
@@ -869,7 +958,8 @@ __global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t np
   __shared__ typename G::Shared gsh;
   __shared__ double red[WARPS];
   G g;
-  g.setup(t, gsh);
+  g.setup(t, gsh, t.dim);
+  __syncthreads();
   const int warp = threadIdx.x >> 5;
   double acc = 0.0;
   for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < npoints;

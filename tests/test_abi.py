@@ -64,6 +64,7 @@ def test_division_magic_is_exact(lib):
         p = int(base[d])
         xs = [0, 1, p - 1, p, p + 1, 2**32 - 1, 2**46 - 1, p**3 - 1 if p**3 < 2**46 else p]
         xs += [int(x) for x in rng.integers(0, 2**46, size=200, dtype=np.int64)]
+        xs += list(range(0, 65536, 997)) + [65535, p * 100 - 1, p * 100]  # 16-bit magic
         for x in xs:
             assert lib.rq_halton_divide(d, x, C.byref(q64), C.byref(q32)) == 0
             assert q64.value == x // p, (d, x)
