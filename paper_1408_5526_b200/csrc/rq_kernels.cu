@@ -863,18 +863,23 @@ __global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
   const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
   const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
   if ((int64_t)blockIdx.x >= total) return;
-  // CTA b owns the contiguous tiles [lo, hi) of the batch (rep-major), so
-  // consecutive tiles of a replication stay on one CTA (persistent
-  // generator state, L1 locality of the replication's tables)
-  const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
-  const int64_t nunit = (hi - lo) * nchunk;
+  // Single-chunk models: CTA b owns the contiguous tiles [lo, hi) of the
+  // batch (rep-major), so consecutive tiles of a replication stay on one CTA
+  // and the generator advances a persistent state.  Multi-chunk models
+  // (long paths, large per-replication tables): tiles are strided over the
+  // CTAs so all CTAs work on the same replication's tables at a time (L2).
+  const bool contiguous = nchunk == 1;
+  const int64_t lo = contiguous ? total * blockIdx.x / gridDim.x : blockIdx.x;
+  const int64_t ntile = contiguous ? total * (blockIdx.x + 1) / gridDim.x - lo
+                                   : (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t nunit = ntile * nchunk;
   // unit cursor: (replication, tile base, chunk) advanced incrementally
   struct Cursor {
     int rl, c;
     int64_t base;
   };
   const int64_t rep_span = a.tiles_per_rep * TILE;
-  const int64_t stride = TILE;
+  const int64_t stride = contiguous ? TILE : (int64_t)gridDim.x * TILE;
   auto advance = [&](Cursor &q) {
     if (++q.c == nchunk) {
       q.c = 0;
