@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "rq_device.cuh"
 #include "rq_internal.h"
@@ -163,12 +164,14 @@ struct RasrapTileShared {
   int32_t hB[CHUNK];               // highest digit where B differs from n0 (-1: B == n0)
   double sJ[CHUNK];                // stream partial sum S_J of the top node
   double lev[WARPS][2][LEVBUF];    // per-warp ping-pong level buffers
-  // persistent stream state (single-chunk models, consecutive tiles of a CTA)
   double P[CHUNK][MAX_CAP + 1];    // S_j(B), j = 0..cap
   int32_t st_rl[CHUNK];            // replication the state belongs to (-1: none)
   uint64_t st_base[CHUNK];         // tile base the state belongs to
   int32_t soff[CHUNK];             // offset of sigma_d in sigd
-  double sigd[SIGD_MAX];           // sigma of the replication's dims as doubles
+};
+// + sigma of a single-chunk model's dims staged as doubles
+struct RasrapTilePersistShared : RasrapTileShared {
+  double sigd[SIGD_MAX];
 };
 struct RasrapDirectShared {
   uint16_t scr[MAX_CAP][TILE];  // per-thread digits (direct path)
@@ -238,8 +241,10 @@ struct GenRasrapRecDirect {
 // That is ~TILE * p/(p-1) node updates per tile and dim instead of
 // TILE * log_p(n) for independent per-point chains, with the same
 // operations in the same order as the reference (bit-identical).
+template <bool PERSIST>
 struct GenRasrapRecTile {
-  using Shared = RasrapTileShared;
+  using Shared = typename std::conditional<PERSIST, RasrapTilePersistShared,
+                                           RasrapTileShared>::type;
   const RepTables *t;
   Shared *sh;
   bool persist;   // consecutive tiles of one CTA share a persistent stream state
@@ -247,7 +252,7 @@ struct GenRasrapRecTile {
   __device__ void setup(const RepTables &t_, Shared &s, int gdims = 0) {
     t = &t_;
     sh = &s;
-    persist = gdims > 0 && gdims <= CHUNK;
+    persist = PERSIST && gdims > 0 && gdims <= CHUNK;
     sig_smem = persist && c_hdim[gdims - 1].sig_off + c_hdim[gdims - 1].base <= SIGD_MAX;
     for (int k = threadIdx.x; k < CHUNK; k += TILE) s.st_rl[k] = -1;
   }
@@ -313,7 +318,7 @@ struct GenRasrapRecTile {
     hB = jmax > hB ? jmax : hB;  // a carry above hB makes that digit exceed n0's
     R.hB[dd] = hB;
     double S = R.P[dd][jmax + 1];
-    const double *sgd = R.sigd + R.soff[dd];
+    const double *sgd = sigd_of(dd);
     const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
 #pragma unroll 1
     for (int k = jmax; k >= 0; k--) {
@@ -321,6 +326,10 @@ struct GenRasrapRecTile {
       S = k > hB ? ini[k] : dadd(S, dmul(sv, w[k]));
       R.P[dd][k] = S;
     }
+  }
+  __device__ __forceinline__ const double *sigd_of(int dd) const {
+    if constexpr (PERSIST) return sh->sigd + sh->soff[dd];
+    return nullptr;
   }
   // per-dim tile state (one lane per dim): digits of B, hB, level sizes, S_J
   __device__ void prepare_dim(int rl, uint64_t base, int d, int dd) {
@@ -346,7 +355,7 @@ struct GenRasrapRecTile {
   }
   __device__ void stage_sigma(int rl, int d0, int Dc) {
     // warp w stages the sigma tables of its dims (dd = w mod WARPS)
-    RasrapTileShared &R = *sh;
+    Shared &R = *sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
     const int off0 = c_hdim[d0].sig_off;
@@ -354,7 +363,8 @@ struct GenRasrapRecTile {
     for (int dd = warp; dd < Dc; dd += WARPS) {
       const HaltonDim &h = c_hdim[d0 + dd];
       const int o = h.sig_off - off0;
-      for (int a = lane; a < h.base; a += 32) R.sigd[o + a] = (double)gsig[h.sig_off + a];
+      if constexpr (PERSIST)
+        for (int a = lane; a < h.base; a += 32) R.sigd[o + a] = (double)gsig[h.sig_off + a];
       if (lane == 0) R.soff[dd] = o;
     }
     __syncwarp();
@@ -375,7 +385,7 @@ struct GenRasrapRecTile {
       const HaltonDim &h = c_hdim[d0 + dd];
       const uint32_t p = (uint32_t)h.base, m16 = h.m16;
       const uint16_t *sg = gsig + h.sig_off;
-      const double *sgd = R.sigd + R.soff[dd];
+      const double *sgd = sigd_of(dd);
       const double *ini = gsum + h.sum_off;
       const double *w = g_wts + h.sum_off;
       const int J = R.J[dd], hB = R.hB[dd];
@@ -389,7 +399,7 @@ struct GenRasrapRecTile {
         const double wj = w[j], inij = ini[j];
         const bool at_n0 = j > hB;  // node 0 of this level has n0's prefix
         double *dst = j ? next : zt + dd * TILE;
-#pragma unroll 2
+#pragma unroll 1
         for (int k = lane; k < Nj; k += 32) {
           const uint32_t x = bj + (uint32_t)k;  // < 2^16
           const uint32_t par = __umulhi(x, m16);
@@ -412,29 +422,33 @@ struct GenRasrapRecTile {
 // multiplication, over max(K, #digits) positions.  The running sum starts
 // at the low digits, so no prefix can be shared across a tile: direct.
 struct GenRasrapCounter {
+  static constexpr int MAXB = 3;  // register-heavy digit loop next to LIBOR(20)
   const RepTables *t;
   using Shared = NoShared;
   __device__ void setup(const RepTables &t_, Shared &, int = 0) { t = &t_; }
-  __device__ __forceinline__ double value(int rl, int d, uint32_t i) const {
-    const HaltonDim &h = c_hdim[d];
-    const uint16_t *d0 = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
-    const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
-    const double *cs = g_cscale + h.sum_off;
-    uint32_t r = i, carry = 0;
-    double x = 0.0;
-    for (int j = 0; j < h.K || r != 0u || carry != 0u; j++) {
-      uint32_t q = div_base(r, h);
-      uint32_t a = d0[j] + (r - q * (uint32_t)h.base) + carry;
-      carry = a >= (uint32_t)h.base;
-      a = carry ? a - (uint32_t)h.base : a;
-      x = dadd(x, dmul(u16d(sg[a]), cs[j]));
-      r = q;
-    }
-    return x;
-  }
   __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
-    for (int dd = 0; dd < Dc; dd++)
-      zt[dd * TILE + threadIdx.x] = value(rl, d0 + dd, (uint32_t)path);
+    const uint16_t *dig = t->digits + (int64_t)rl * t->dig_stride;
+    const uint16_t *sig = t->sigma + (int64_t)rl * t->sig_stride;
+    const uint32_t i = (uint32_t)path;
+#pragma unroll 1
+    for (int dd = 0; dd < Dc; dd++) {
+      const HaltonDim &h = c_hdim[d0 + dd];
+      const uint16_t *n0d = dig + h.dig_off;
+      const uint16_t *sg = sig + h.sig_off;
+      const double *cs = g_cscale + h.sum_off;
+      uint32_t r = i, carry = 0;
+      double x = 0.0;
+#pragma unroll 1
+      for (int j = 0; j < h.K || r != 0u || carry != 0u; j++) {
+        uint32_t q = div_base(r, h);
+        uint32_t a = n0d[j] + (r - q * (uint32_t)h.base) + carry;
+        carry = a >= (uint32_t)h.base;
+        a = carry ? a - (uint32_t)h.base : a;
+        x = dadd(x, dmul(u16d(sg[a]), cs[j]));
+        r = q;
+      }
+      zt[dd * TILE + threadIdx.x] = x;
+    }
   }
 };
 
@@ -846,8 +860,19 @@ struct PathArgs {
 
 constexpr size_t ZT_BYTES = sizeof(double) * CHUNK * TILE;  // one uniform/normal tile
 
+template <class G>
+struct MaxBlocks {  // optional per-generator cap on CTAs/SM (register budget)
+  template <class T>
+  static constexpr int get(decltype(T::MAXB) *) { return T::MAXB; }
+  template <class T>
+  static constexpr int get(...) { return 8; }
+  static constexpr int value = get<G>(nullptr);
+};
+
 template <class G, class Mdl>
-__global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
+__global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::MINB
+                                                                          : MaxBlocks<G>::value))
+    k_paths(PathArgs a) {
   extern __shared__ __align__(16) double zdyn[];  // 2 x ZT_BYTES (double buffer)
   auto zbuf = [&](int64_t u) { return zdyn + (u & 1) * (CHUNK * TILE); };
   __shared__ uint16_t tq[WARPS][CHUNK * 32];
@@ -861,51 +886,53 @@ __global__ void __launch_bounds__(TILE, Mdl::MINB) k_paths(PathArgs a) {
   g.setup(a.t, gsh, gdims);
   __syncthreads();
   const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
-  const int64_t total = (int64_t)a.rep_n * a.tiles_per_rep;
-  if ((int64_t)blockIdx.x >= total) return;
+  // tiles per launch <= (payoff batch 2^25 paths) / TILE: 32-bit counters
+  const int total = a.rep_n * (int)a.tiles_per_rep;
+  if ((int)blockIdx.x >= total) return;
   // Single-chunk models: CTA b owns the contiguous tiles [lo, hi) of the
   // batch (rep-major), so consecutive tiles of a replication stay on one CTA
   // and the generator advances a persistent state.  Multi-chunk models
   // (long paths, large per-replication tables): tiles are strided over the
   // CTAs so all CTAs work on the same replication's tables at a time (L2).
   const bool contiguous = nchunk == 1;
-  const int64_t lo = contiguous ? total * blockIdx.x / gridDim.x : blockIdx.x;
-  const int64_t ntile = contiguous ? total * (blockIdx.x + 1) / gridDim.x - lo
-                                   : (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t nunit = ntile * nchunk;
-  // unit cursor: (replication, tile base, chunk) advanced incrementally
+  const int nb = gridDim.x, b = blockIdx.x;
+  const int lo = contiguous ? (int)((int64_t)total * b / nb) : b;
+  const int ntile =
+      contiguous ? (int)((int64_t)total * (b + 1) / nb) - lo : (total - b + nb - 1) / nb;
+  const int nunit = ntile * nchunk;
+  // unit cursor: (replication, tile, chunk) advanced incrementally
   struct Cursor {
-    int rl, c;
-    int64_t base;
+    int rl, c, tile;
   };
-  const int64_t rep_span = a.tiles_per_rep * TILE;
-  const int64_t stride = contiguous ? TILE : (int64_t)gridDim.x * TILE;
+  const int tpr = (int)a.tiles_per_rep;
+  const int tstride = contiguous ? 1 : nb;
   auto advance = [&](Cursor &q) {
     if (++q.c == nchunk) {
       q.c = 0;
-      q.base += stride;
-      while (q.base >= rep_span) {
-        q.base -= rep_span;
+      q.tile += tstride;
+      while (q.tile >= tpr) {
+        q.tile -= tpr;
         q.rl++;
       }
     }
   };
-  Cursor cur{a.rep_local0 + (int)(lo / a.tiles_per_rep), 0,
-             (int64_t)(lo % a.tiles_per_rep) * TILE};
+  Cursor cur{a.rep_local0 + lo / tpr, 0, lo % tpr};
   auto dc_of = [&](int c) { return gdims - c * CHUNK < CHUNK ? gdims - c * CHUNK : CHUNK; };
+  auto base_of = [&](const Cursor &q) { return (int64_t)q.tile * TILE; };
   if (RQ_PIPELINE && gdims > 0)
-    g.unit(cur.rl, (uint64_t)cur.base, (uint64_t)(cur.base + threadIdx.x), 0, dc_of(0), zbuf(0));
+    g.unit(cur.rl, (uint64_t)base_of(cur), (uint64_t)(base_of(cur) + threadIdx.x), 0, dc_of(0),
+           zbuf(0));
   __syncthreads();
-  for (int64_t u = 0; u < nunit; u++) {
+  for (int u = 0; u < nunit; u++) {
     Cursor nxt = cur;
     advance(nxt);
     const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
-    const int64_t base = cur.base;
+    const int64_t base = base_of(cur);
     double *z = zbuf(RQ_PIPELINE ? u : 0);
     if (RQ_PIPELINE) {
       if (gdims > 0 && u + 1 < nunit)  // generate the next unit into the other buffer
-        g.unit(nxt.rl, (uint64_t)nxt.base, (uint64_t)(nxt.base + threadIdx.x), nxt.c * CHUNK,
-               dc_of(nxt.c), zbuf(u + 1));
+        g.unit(nxt.rl, (uint64_t)base_of(nxt), (uint64_t)(base_of(nxt) + threadIdx.x),
+               nxt.c * CHUNK, dc_of(nxt.c), zbuf(u + 1));
     } else if (gdims > 0) {
       g.unit(rl, (uint64_t)base, (uint64_t)(base + threadIdx.x), d0, Dc, z);
       __syncthreads();
@@ -1169,7 +1196,7 @@ cudaError_t launch_points(const RepTables &t, int rl, int64_t first, const int64
   switch (t.gen) {
     case GEN_RASRAP_RECURSIVE:
       return at ? points_t<GenRasrapRecDirect>(t, rl, first, idx, count, out, s)
-                : points_t<GenRasrapRecTile>(t, rl, first, idx, count, out, s);
+                : points_t<GenRasrapRecTile<false>>(t, rl, first, idx, count, out, s);
     case GEN_RASRAP_COUNTER: return points_t<GenRasrapCounter>(t, rl, first, idx, count, out, s);
     case GEN_PHILOX: return points_t<GenPhilox>(t, rl, first, idx, count, out, s);
     case GEN_SOBOL_GRAY:
@@ -1220,7 +1247,10 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
 static cudaError_t paths_dispatch(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                                   int *blocks) {
   switch (a.t.gen) {
-    case GEN_RASRAP_RECURSIVE: return paths_g<GenRasrapRecTile>(a, launched, s, probe, blocks);
+    case GEN_RASRAP_RECURSIVE:
+      return a.mp.kind == MODEL_MBS || a.mp.dim > CHUNK
+                 ? paths_g<GenRasrapRecTile<false>>(a, launched, s, probe, blocks)
+                 : paths_g<GenRasrapRecTile<true>>(a, launched, s, probe, blocks);
     case GEN_RASRAP_COUNTER: return paths_g<GenRasrapCounter>(a, launched, s, probe, blocks);
     case GEN_PHILOX: return paths_g<GenPhilox>(a, launched, s, probe, blocks);
     case GEN_SOBOL_GRAY: return paths_g<GenSobolTile<true>>(a, launched, s, probe, blocks);
@@ -1304,7 +1334,7 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
                                   cudaStream_t s) {
   switch (t.gen) {
     case GEN_RASRAP_RECURSIVE:
-      return stream_t<GenRasrapRecTile>(t, rl, npoints, block_sums, nblocks, store, s);
+      return stream_t<GenRasrapRecTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_RASRAP_COUNTER:
       return stream_t<GenRasrapCounter>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_PHILOX: return stream_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
