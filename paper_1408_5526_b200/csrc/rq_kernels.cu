@@ -399,14 +399,20 @@ struct GenRasrapRecTile {
         const double wj = w[j], inij = ini[j];
         const bool at_n0 = j > hB;  // node 0 of this level has n0's prefix
         double *dst = j ? next : zt + dd * TILE;
-#pragma unroll 1
-        for (int k = lane; k < Nj; k += 32) {
+        auto node = [&](int k) {
           const uint32_t x = bj + (uint32_t)k;  // < 2^16
           const uint32_t par = __umulhi(x, m16);
           const uint32_t a = x - par * p;
           const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
           double v = dadd(prev[par], dmul(sv, wj));
           dst[k] = (at_n0 && k == 0) ? inij : v;
+        };
+        if constexpr (PERSIST) {  // sigma in shared memory
+#pragma unroll 1
+          for (int k = lane; k < Nj; k += 32) node(k);
+        } else {  // sigma from L2: keep several lookups in flight
+#pragma unroll 4
+          for (int k = lane; k < Nj; k += 32) node(k);
         }
         __syncwarp();
         double *tmp = prev;
