@@ -205,11 +205,10 @@ def run_ours(args) -> dict:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
+    use_dist = "RANK" in os.environ  # launched by torchrun (any world size)
+    torch.cuda.set_device(local)
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
     lib = _lib.lib()
     kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
     if args.reps:
@@ -225,13 +224,13 @@ def run_ours(args) -> dict:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
     def one_step():
         h, n, keep = device_step(gen_id, model, SEED, first, M, grid, theta, lib, C, _lib)
-        if world > 1:
+        if use_dist:  # the one collective: theta of every rank, once per step
             dist.all_gather(gathered, theta)
         return h, n
 
@@ -258,7 +257,7 @@ def run_ours(args) -> dict:
     clk = clocks.stop()
     ms = float(np.mean(step_ms))
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if use_dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     paths = M * N * world
@@ -285,7 +284,7 @@ def run_ours(args) -> dict:
     tr = _lib.stats_get()
     ne = len(e2e_ms)
     e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if use_dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = paths / (float(e2e_t.item()) * 1e-3)
 
@@ -306,7 +305,9 @@ def run_ours(args) -> dict:
             "data": "synthetic (seed 20120224, replication ids from 1, packaged 2012-02-24 "
                     "Treasury curve)",
             "config": {"workload": desc, "generator": gen, "M_per_gpu": M, "N": N,
-                       "model": kind, "dim": model.dim, "parallelism": f"replications x{world}",
+                       "model": kind, "dim": model.dim,
+                       "parallelism": f"replication-sharded x{world} (theta all-gathered once "
+                                      f"per step{' over NCCL' if use_dist else ''})",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "roofline": {
                 "bound": "fp64",
@@ -331,7 +332,7 @@ def run_ours(args) -> dict:
         }
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(model, gen, N, args)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return out
