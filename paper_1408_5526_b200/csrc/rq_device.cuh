@@ -282,9 +282,18 @@ __device__ __forceinline__ double invn_fold(double p, bool *neg) {
   return pl < InvNormal::TINY ? InvNormal::TINY : pl;
 }
 __device__ __forceinline__ double invn_central(double pl) {
-  double q = pl - 0.5;
-  double u = (q * q) * (1.0 / InvNormal::RMAX);
-  return q * invn_central_num(u) * rcp2(invn_central_den(u));
+  // the reference rational in u = q^2 / R (models.py:51-56) with the 1/R^k
+  // folded into the coefficients, so the polynomials run directly in q^2
+  const double q = pl - 0.5, s = q * q;
+  const double num =
+      ((((((-18758.264827117993 * s + 121493.75753172635) * s + -169742.25554056765) * s +
+          95028.92000917176) * s + -24309.66331940731) * s + 2693.622228066229) * s +
+       -105.1488511356405) * s + 3.8841077977297096;
+  const double den =
+      ((((((-27571.106587154845 * s + 92106.19422816113) * s + -98233.8844955836) * s +
+          46868.23917353603) * s + -10776.85973982955) * s + 1116.658786813825) * s +
+       -43.57099147618938) * s + 1.5495348220676615;
+  return (q * num) * rcp1(den);
 }
 __device__ __forceinline__ double invn_tail(double pl) {
   double w = (sqrt(-2.0 * log(pl)) - InvNormal::VLO) * InvNormal::VSCALE;

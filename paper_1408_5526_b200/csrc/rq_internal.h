@@ -6,7 +6,7 @@
 
 namespace rq {
 
-constexpr int MAX_DIM = 1024;   // Halton/Rasrap dimensions with universal tables
+constexpr int MAX_DIM = 512;    // Halton/Rasrap dimensions with universal tables
 constexpr int MAX_CAP = 40;     // K + 8 for base 2 (largest digit window)
 constexpr int SOBOL_BITS = 32;  // sobol.py:30
 constexpr int CHUNK_DIMS = 20;  // dimensions per generator chunk in the fused kernels

@@ -44,6 +44,8 @@ constexpr double TWO_M33 = 1.1641532182693481e-10;  // 2^-33
 constexpr double TWO_M53 = 1.1102230246251565e-16;  // 2^-53
 
 __constant__ HaltonDim c_hdim[MAX_DIM];
+constexpr int CWTS = 1280;  // binpow weights of the first dims, in the constant bank
+__constant__ double c_wts[CWTS];
 constexpr int WTS_CAP = 16384;
 __device__ double g_wts[WTS_CAP];     // binpow(inv_p, j+1): numba `x ** int` (halton.py:409)
 __device__ double g_cscale[WTS_CAP];  // counter-form scale chain (halton.py:436)
@@ -54,6 +56,8 @@ cudaError_t upload_halton_dims(const HaltonDim *dims, int n, const double *wts,
   cudaError_t e = cudaMemcpyToSymbol(c_hdim, dims, sizeof(HaltonDim) * n);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyToSymbol(g_wts, wts, sizeof(double) * nw);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyToSymbol(c_wts, wts, sizeof(double) * (nw < CWTS ? nw : CWTS));
   if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(g_cscale, cscale, sizeof(double) * nw);
 }
@@ -387,37 +391,42 @@ struct GenRasrapRecTile {
       const uint16_t *sg = gsig + h.sig_off;
       const double *sgd = sigd_of(dd);
       const double *ini = gsum + h.sum_off;
+      const bool cw = h.sum_off + h.cap < CWTS;  // weights in the constant bank
       const double *w = g_wts + h.sum_off;
       const int J = R.J[dd], hB = R.hB[dd];
       double *prev = R.lev[warp][0], *next = R.lev[warp][1];
       if (lane == 0) prev[0] = R.sJ[dd];
       __syncwarp();
+      // one node: S_j(prefix) = S_{j+1}(parent) + sigma(digit) * w_j, or the
+      // init sum when the prefix is n0's (node 0 of a level above hB)
+      auto node = [&](uint32_t bj, int k, double wj, bool at_n0, int j, double *dst) {
+        const uint32_t x = bj + (uint32_t)k;  // < 2^16
+        const uint32_t par = __umulhi(x, m16);
+        const uint32_t a = x - par * p;
+        const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
+        double v = dadd(prev[par], dmul(sv, wj));
+        if (at_n0 && k == 0) v = ini[j];
+        dst[k] = v;
+      };
 #pragma unroll 1
-      for (int j = J - 1; j >= 0; j--) {
+      for (int j = J - 1; j >= 1; j--) {  // upper levels: <= TILE/2 + 2 nodes
         const int Nj = R.nn[dd][j];
         const uint32_t bj = R.bd[dd][j];
-        const double wj = w[j], inij = ini[j];
-        const bool at_n0 = j > hB;  // node 0 of this level has n0's prefix
-        double *dst = j ? next : zt + dd * TILE;
-        auto node = [&](int k) {
-          const uint32_t x = bj + (uint32_t)k;  // < 2^16
-          const uint32_t par = __umulhi(x, m16);
-          const uint32_t a = x - par * p;
-          const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
-          double v = dadd(prev[par], dmul(sv, wj));
-          dst[k] = (at_n0 && k == 0) ? inij : v;
-        };
-        if constexpr (PERSIST) {  // sigma in shared memory
+        const double wj = cw ? c_wts[h.sum_off + j] : w[j];
+        const bool at_n0 = j > hB;
 #pragma unroll 1
-          for (int k = lane; k < Nj; k += 32) node(k);
-        } else {  // sigma from L2: keep several lookups in flight
-#pragma unroll 4
-          for (int k = lane; k < Nj; k += 32) node(k);
-        }
+        for (int k = lane; k < Nj; k += 32) node(bj, k, wj, at_n0, j, next);
         __syncwarp();
         double *tmp = prev;
         prev = next;
         next = tmp;
+      }
+      {  // level 0: the TILE points
+        const uint32_t b0 = R.bd[dd][0];
+        const double w0 = cw ? c_wts[h.sum_off] : w[0];
+        const bool at_n0 = 0 > hB;
+#pragma unroll
+        for (int m = 0; m < TILE / 32; m++) node(b0, lane + 32 * m, w0, at_n0, 0, zt + dd * TILE);
       }
     }
   }

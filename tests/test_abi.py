@@ -46,8 +46,8 @@ def test_library_exports_every_declared_symbol(lib):
 def test_halton_constants_match_reference(lib, oracle):
     from paper_1408_5526_b200.tables import halton_constants
 
-    base, K, scale0 = halton_constants(1024)
-    assert np.array_equal(base, oracle.primes(1024))
+    base, K, scale0 = halton_constants(512)
+    assert np.array_equal(base, oracle.primes(512))
     for p, k, s in zip(base, K, scale0):
         p, k = int(p), int(k)
         assert p**k >= 2**32 > p ** (k - 1)  # digit_capacity, halton.py:59-66
@@ -57,10 +57,10 @@ def test_halton_constants_match_reference(lib, oracle):
 def test_division_magic_is_exact(lib):
     from paper_1408_5526_b200.tables import halton_constants
 
-    base, _, _ = halton_constants(1024)
+    base, _, _ = halton_constants(512)
     rng = np.random.default_rng(3)
     q64, q32 = C.c_uint64(), C.c_uint32()
-    for d in list(range(40)) + list(range(40, 1024, 37)) + [1023]:
+    for d in list(range(40)) + list(range(40, 512, 37)) + [511]:
         p = int(base[d])
         xs = [0, 1, p - 1, p, p + 1, 2**32 - 1, 2**46 - 1, p**3 - 1 if p**3 < 2**46 else p]
         xs += [int(x) for x in rng.integers(0, 2**46, size=200, dtype=np.int64)]
