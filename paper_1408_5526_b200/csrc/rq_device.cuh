@@ -293,7 +293,9 @@ __device__ __forceinline__ double invn_central(double pl) {
       ((((((-27571.106587154845 * s + 92106.19422816113) * s + -98233.8844955836) * s +
           46868.23917353603) * s + -10776.85973982955) * s + 1116.658786813825) * s +
        -43.57099147618938) * s + 1.5495348220676615;
-  return (q * num) * rcp1(den);
+  // quotient: one-Newton reciprocal (~2^-40) then one residual correction
+  const double n = q * num, r = rcp1(den), y = n * r;
+  return fma(r, fma(-den, y, n), y);
 }
 __device__ __forceinline__ double invn_tail(double pl) {
   double w = (sqrt(-2.0 * log(pl)) - InvNormal::VLO) * InvNormal::VSCALE;
