@@ -20,7 +20,7 @@ HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "build" / "librqmc_oracle.so"
 
 GEN_IDS = {"rasrap-recursive": 0, "rasrap-counter": 1, "philox": 2, "sobol-gray": 3,
-           "sobol-counter": 4}
+           "sobol-counter": 4, "sfc64": 5}
 MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3}
 FAMILY_IDS = {"twister": 1, "xorwow": 2, "philox": 3, "rasrap": 4, "sobol": 5, "kakutani": 6,
               "sfc64": 7}

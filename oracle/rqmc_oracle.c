@@ -664,12 +664,12 @@ void orc_sfc64_path_uniforms(uint64_t seed, int64_t m, const int64_t *paths, int
 
 #define CHUNK_PATHS 8192 /* harness.py:25 */
 
-static const uint64_t FAMILY_ID[5] = {4, 4, 3, 5, 5}; /* seeding.py:17-24 */
+static const uint64_t FAMILY_ID[6] = {4, 4, 3, 5, 5, 7}; /* seeding.py:17-24; 7 = sfc64 */
 
 int orc_run_replication(int gen, int model, int dim, const double *mparams, uint64_t seed,
                         int64_t m, const int64_t *grid, int ngrid, const uint32_t *sobol_v,
                         double *theta) {
-  if (gen < 0 || gen > 4 || model < 0 || model > 3 || ngrid < 1) return -1;
+  if (gen < 0 || gen > 5 || model < 0 || model > 3 || ngrid < 1) return -1;
   int64_t nmax = grid[ngrid - 1];
   uint64_t parts[3] = {seed, FAMILY_ID[gen], (uint64_t)m};
   uint64_t key = orc_derive_key(parts, 3); /* harness.py:113 */
@@ -694,6 +694,8 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
       rec_fill(&rec, cnt, buf);
     } else if (gen == 1) {
       counter_points(&cfg, idx, cnt, buf);
+    } else if (gen == 5) {
+      orc_sfc64_path_uniforms(seed, m, idx, cnt, dim, buf);
     } else if (gen == 2) {
       orc_philox_words(key, idx, cnt, dim, words);
       for (int64_t i = 0; i < cnt * dim; i++)

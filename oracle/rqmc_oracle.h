@@ -87,7 +87,7 @@ double orc_pairwise_sum(const double *a, int64_t n);
 /* One full replication (harness.py:291-315): generator -> model -> prefix
  * estimates theta[g] = np.sum(payoffs[:grid[g]]) / grid[g].
  * gen: 0 rasrap-recursive, 1 rasrap-counter, 2 philox, 3 sobol-gray,
- *      4 sobol-counter.  model: 0 libor, 1 mbs, 2 x1, 3 const1.
+ *      4 sobol-counter, 5 sfc64 (builder-defined per-path streams).  model: 0 libor, 1 mbs, 2 x1, 3 const1.
  * mparams: libor {delta, sigma, strike, front_factor, l0[steps]...};
  *          mbs {i0,k0,k1,k2,k3,k4,sigma_xi,payment, ck[months]...}.
  * sobol_v: unscrambled direction words [dim x 32] (gen 3/4 only). */

@@ -339,3 +339,83 @@ def test_errors_map_to_reference_exceptions(P):
 
     with pytest.raises(ValueError):
         M.LiborModel().payoffs(np.zeros((3, 4)))
+
+
+# ---------------------------------------------------------------- edge cases vs the oracle
+def _oracle_theta(oracle, gen, model, seed, first, count, grid):
+    sob = None
+    if gen.startswith("sobol"):
+        from paper_1408_5526_b200.tables import sobol_directions
+
+        sob = sobol_directions(model.dim)
+    return oracle.run_replications(gen, model, seed, first, count, grid, threads=8, sobol_v=sob)
+
+
+@pytest.mark.parametrize("gen", ["rasrap-recursive", "rasrap-counter", "philox", "sobol-gray",
+                                 "sobol-counter", "sfc64"])
+def test_ragged_grids_and_big_ids(P, oracle, gen):
+    """N not a multiple of the 128-path tile, N = 1, several grid points,
+    replication ids far from 1, a 64-bit seed: theta vs the oracle."""
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    model = M.LiborModel(M.LiborConfig(maturity=5.0, accrual=0.25))
+    grid = (1, 2, 7, 127, 129, 1000, 4099)
+    for seed, first in ((SEED, 1), (2**63 + 12345, 1_000_003)):
+        got = estimate_replications(gen, model, seed, first, 3, grid)
+        ref = _oracle_theta(oracle, gen, model, seed, first, 3, grid)
+        scale = np.maximum(np.abs(ref), 1e-3 * np.abs(ref).max())
+        assert (np.abs(got - ref) / scale).max() <= THETA_RTOL, (seed, first)
+
+
+@pytest.mark.parametrize("mat,acc", [(5.0, 0.5), (10.0, 0.25), (20.0, 0.25)])
+def test_libor_steps_vs_oracle(P, oracle, mat, acc):
+    """All compiled LIBOR widths (S = 10, 40, 80) through the fused kernel."""
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    model = M.LiborModel(M.LiborConfig(maturity=mat, accrual=acc))
+    for gen in ("rasrap-recursive", "philox"):
+        got = estimate_replications(gen, model, SEED, 5, 2, (3000,))
+        ref = _oracle_theta(oracle, gen, model, SEED, 5, 2, (3000,))
+        assert (np.abs(got / ref - 1)).max() <= THETA_RTOL
+
+
+@pytest.mark.parametrize("cfg", [dict(months=24), dict(months=360, variance=0.0),
+                                 dict(months=100, variance=0.0009, initial_rate=0.01)])
+def test_mbs_variants_vs_oracle(P, oracle, cfg):
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    model = M.MbsModel(M.MbsConfig(**cfg))
+    for gen in ("rasrap-recursive", "sobol-gray"):
+        got = estimate_replications(gen, model, SEED, 1, 2, (777,))
+        ref = _oracle_theta(oracle, gen, model, SEED, 1, 2, (777,))
+        assert (np.abs(got / ref - 1)).max() <= THETA_RTOL
+
+
+def test_x1_dim1_and_const_bit_exact(P, oracle):
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    for gen in ("rasrap-recursive", "sobol-gray", "philox", "sfc64", "rasrap-counter"):
+        m = M.FirstCoordinateModel(dim=1)
+        got = estimate_replications(gen, m, SEED, 1, 4, (5, 128, 131, 70_001))
+        ref = _oracle_theta(oracle, gen, m, SEED, 1, 4, (5, 128, 131, 70_001))
+        assert np.array_equal(got, ref), gen
+    c = estimate_replications("philox", M.ConstantModel(), SEED, 1, 3, (9, 1000))
+    assert np.all(c == 1.0)
+
+
+def test_many_replications_batched(P, oracle):
+    """More replications than one payoff batch / sampler group: theta of a
+    500-replication run equals per-replication oracle values."""
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    m = M.FirstCoordinateModel()
+    got = estimate_replications("rasrap-recursive", m, SEED, 1, 500, (300_000,))
+    idx = [0, 1, 137, 255, 256, 499]
+    for i in idx:
+        ref = _oracle_theta(oracle, "rasrap-recursive", m, SEED, 1 + i, 1, (300_000,))
+        assert got[i, 0] == ref[0, 0]
