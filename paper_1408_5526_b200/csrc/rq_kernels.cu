@@ -339,7 +339,11 @@ struct GenRasrapRecTile {
   __device__ void prepare_dim(int rl, uint64_t base, int d, int dd) {
     RasrapTileShared &R = *sh;
     const HaltonDim &h = c_hdim[d];
-    if (persist && R.st_rl[dd] == rl && R.st_base[dd] + TILE == base) {
+    if (!persist) {  // stateless: digits up to the top level, S_J by one chain
+      prepare_stateless(rl, base, d, dd);
+      return;
+    }
+    if (R.st_rl[dd] == rl && R.st_base[dd] + TILE == base) {
       state_advance(rl, d, dd);
     } else {
       state_full(rl, base, d, dd);
@@ -356,6 +360,44 @@ struct GenRasrapRecTile {
     }
     R.J[dd] = J;
     R.sJ[dd] = R.P[dd][J];
+  }
+  __device__ void prepare_stateless(int rl, uint64_t base, int d, int dd) {
+    RasrapTileShared &R = *sh;
+    const HaltonDim &h = c_hdim[d];
+    const uint32_t p = (uint32_t)h.base;
+    const uint16_t *n0d = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
+    const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
+    const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
+    const double *w = g_wts + h.sum_off;
+    const uint64_t n0 = t->start[(int64_t)rl * t->dim + d];
+    uint64_t qb = n0 + base, qn = n0;
+    int j = 0, hB = -1;
+#pragma unroll 1
+    while (qb != qn) {  // positions where B's prefix still differs from n0's
+      uint64_t nb = div_base64(qb, h), nq = div_base64(qn, h);
+      uint32_t db = (uint32_t)(qb - nb * p), dn = (uint32_t)(qn - nq * p);
+      R.bd[dd][j] = (uint16_t)db;
+      hB = db != dn ? j : hB;
+      qb = nb;
+      qn = nq;
+      j++;
+    }
+    int N = TILE, J = 0;
+    R.nn[dd][0] = (int16_t)N;
+#pragma unroll 1
+    while (N > 1) {
+      uint32_t bj = J < j ? R.bd[dd][J] : n0d[J];
+      if (J >= j) R.bd[dd][J] = (uint16_t)bj;
+      N = (int)__umulhi(bj + (uint32_t)N - 1u, h.m16) + 1;
+      J++;
+      R.nn[dd][J] = (int16_t)N;
+    }
+    double S = ini[hB + 1 > J ? hB + 1 : J];
+#pragma unroll 1
+    for (int k = hB; k >= J; k--) S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
+    R.J[dd] = J;
+    R.hB[dd] = hB;
+    R.sJ[dd] = S;
   }
   __device__ void stage_sigma(int rl, int d0, int Dc) {
     // warp w stages the sigma tables of its dims (dd = w mod WARPS)
