@@ -516,6 +516,13 @@ static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, doub
   mp.k4 = m->k4;
   mp.sigma_xi = m->sigma_xi;
   mp.payment = m->payment;
+  // k0 * exp(sigma_xi z) = sum_k (k0 sigma_xi^k / k!) z^k for |sigma_xi z| <= 0.1
+  double c = m->k0;
+  for (int k = 0; k < rq::MBS_EXP_TERMS; k++) {
+    mp.ecoef[k] = c;
+    c = c * m->sigma_xi / (double)(k + 1);
+  }
+  mp.exp_zlim = m->sigma_xi > 0.0 ? 0.1 / m->sigma_xi : INFINITY;
   mp.table = nullptr;
   *tab_dev = nullptr;
   if (m->kind == rq::MODEL_LIBOR || m->kind == rq::MODEL_MBS) {

@@ -219,7 +219,7 @@ RQ_HD void sfc_seed(Sfc64 &s, uint64_t path_key) {
 }
 
 // ---------------------------------------------------------------- division helpers
-// Fast reciprocal: MUFU.RCP64H seed + Newton.  One step leaves ~2^-44
+// Fast reciprocal: MUFU.RCP64H seed (~2^-20) + Newton.  One step leaves ~2^-40
 // relative error, two steps ~1 ulp.
 #if defined(__CUDACC__)
 __device__ __forceinline__ double rcp_seed(double x) {
@@ -231,6 +231,13 @@ __device__ __forceinline__ double rcp1(double x) {
   double r = rcp_seed(x);
   double e = fma(-x, r, 1.0);
   return fma(r, e, r);
+}
+// n / d by two residual corrections of the MUFU seed r0 (~2^-20):
+// y1 = y0 + r0 (n - d y0) has relative error ~eps^2 ~ 1e-12, y2 ~eps^3.
+__device__ __forceinline__ double div2(double n, double d) {
+  const double r0 = rcp_seed(d), y0 = n * r0;
+  const double y1 = fma(r0, fma(-d, y0, n), y0);
+  return fma(r0, fma(-d, y1, n), y1);
 }
 __device__ __forceinline__ double rcp2(double x) {
   double r = rcp_seed(x);
@@ -281,10 +288,23 @@ __device__ __forceinline__ double invn_fold(double p, bool *neg) {
   double pl = *neg ? 1.0 - p : p;
   return pl < InvNormal::TINY ? InvNormal::TINY : pl;
 }
-__device__ __forceinline__ double invn_central(double pl) {
-  // the reference rational in u = q^2 / R (models.py:51-56) with the 1/R^k
-  // folded into the coefficients, so the polynomials run directly in q^2
-  const double q = pl - 0.5, s = q * q;
+// Tail test straight on the bit pattern of p in [0, 1): the reference takes
+// the tail when fold(p) < PLOW (models.py:41-45), i.e. p < PLOW or
+// 1 - p < PLOW; 1 - p is exact for p > 1/2, so the second is p > HI with
+// HI = the largest double <= 1 - PLOW (real).  One unsigned range check.
+constexpr uint64_t INVN_PLOW_BITS = 0x3fa7ced916872b02ULL;  // 0.0465
+constexpr uint64_t INVN_HI_BITS = 0x3fee83126e978d4fULL;    // floor_double(1 - 0.0465)
+__device__ __forceinline__ bool invn_tail_p(double p) {
+  return (uint64_t)__double_as_longlong(p) - INVN_PLOW_BITS > INVN_HI_BITS - INVN_PLOW_BITS;
+}
+// Central branch on Q = p - 1/2 without folding.  For p > 1/2 the
+// reference computes q = (1 - p) - 1/2 = 1/2 - p exactly (Sterbenz) and
+// returns -(q R(q^2)) = Q R(Q^2); for p <= 1/2, Q is the reference's own
+// q = fl(p - 1/2).  R is the reference rational in u = q^2 / R_MAX
+// (models.py:46-54) with the 1/R_MAX^k folded into the coefficients, so the
+// polynomials run directly in Q^2.
+__device__ __forceinline__ double invn_central_q(double Q) {
+  const double s = Q * Q;
   const double num =
       ((((((-18758.264827117993 * s + 121493.75753172635) * s + -169742.25554056765) * s +
           95028.92000917176) * s + -24309.66331940731) * s + 2693.622228066229) * s +
@@ -293,19 +313,18 @@ __device__ __forceinline__ double invn_central(double pl) {
       ((((((-27571.106587154845 * s + 92106.19422816113) * s + -98233.8844955836) * s +
           46868.23917353603) * s + -10776.85973982955) * s + 1116.658786813825) * s +
        -43.57099147618938) * s + 1.5495348220676615;
-  // quotient: one-Newton reciprocal (~2^-40) then one residual correction
-  const double n = q * num, r = rcp1(den), y = n * r;
-  return fma(r, fma(-den, y, n), y);
+  return div2(Q * num, den);
 }
+__device__ __forceinline__ double invn_central(double pl) { return invn_central_q(pl - 0.5); }
 __device__ __forceinline__ double invn_tail(double pl) {
   double w = (sqrt(-2.0 * log(pl)) - InvNormal::VLO) * InvNormal::VSCALE;
   return invn_tail_num(w) * rcp2(invn_tail_den(w));
 }
 // Scalar Phi^-1 (divergent tail); the tile filler uses a compacted tail.
 __device__ __forceinline__ double inv_normal(double p) {
+  if (!invn_tail_p(p)) return invn_central_q(p - 0.5);
   bool neg;
-  double pl = invn_fold(p, &neg);
-  double x = pl >= InvNormal::PLOW ? invn_central(pl) : invn_tail(pl);
+  double x = invn_tail(invn_fold(p, &neg));
   return neg ? -x : x;
 }
 #endif

@@ -10,6 +10,7 @@ constexpr int MAX_DIM = 512;    // Halton/Rasrap dimensions with universal table
 constexpr int MAX_CAP = 40;     // K + 8 for base 2 (largest digit window)
 constexpr int SOBOL_BITS = 32;  // sobol.py:30
 constexpr int CHUNK_DIMS = 20;  // dimensions per generator chunk in the fused kernels
+constexpr int MBS_EXP_TERMS = 10;  // k0 exp(sigma_xi z) polynomial: z^0 .. z^9
 
 enum Gen : int {
   GEN_RASRAP_RECURSIVE = 0,
@@ -64,6 +65,10 @@ struct ModelParams {
   double delta, sigma, strike, front_factor;          // LIBOR (models.py:301-322)
   double i0, k0, k1, k2, k3, k4, sigma_xi, payment;   // MBS (models.py:337-370)
   const double *table;  // device: LIBOR l0[dim] / MBS ck[dim]
+  // MBS: k0 sigma_xi^k / k!, k < MBS_EXP_TERMS (the kernel's k0 exp(sigma_xi z)
+  // for |z| <= exp_zlim = 0.1 / sigma_xi)
+  double ecoef[MBS_EXP_TERMS];
+  double exp_zlim;
 };
 
 // numpy pairwise-sum plan for one N (see rq_capi.cu build_plan).

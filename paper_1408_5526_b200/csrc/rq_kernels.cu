@@ -168,13 +168,14 @@ struct RasrapTileShared {
   int32_t hB[CHUNK];               // highest digit where B differs from n0 (-1: B == n0)
   double sJ[CHUNK];                // stream partial sum S_J of the top node
   double lev[WARPS][2][LEVBUF];    // per-warp ping-pong level buffers
-  double P[CHUNK][MAX_CAP + 1];    // S_j(B), j = 0..cap
   int32_t st_rl[CHUNK];            // replication the state belongs to (-1: none)
   uint64_t st_base[CHUNK];         // tile base the state belongs to
   int32_t soff[CHUNK];             // offset of sigma_d in sigd
 };
-// + sigma of a single-chunk model's dims staged as doubles
+// + the persistent partial sums and sigma of a single-chunk model's dims
+// staged as doubles
 struct RasrapTilePersistShared : RasrapTileShared {
+  double P[CHUNK][MAX_CAP + 1];  // S_j(B), j = 0..cap
   double sigd[SIGD_MAX];
 };
 struct RasrapDirectShared {
@@ -263,7 +264,7 @@ struct GenRasrapRecTile {
   // Full state at B = n0 + base: digits, hB, P[j] = S_j(B) (chain from
   // init_sums[hB+1]); used for a CTA's first tile of a replication.
   __device__ void state_full(int rl, uint64_t base, int d, int dd) {
-    RasrapTileShared &R = *sh;
+    Shared &R = *sh;
     const HaltonDim &h = c_hdim[d];
     const uint32_t p = (uint32_t)h.base;
     const uint16_t *n0d = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
@@ -299,7 +300,7 @@ struct GenRasrapRecTile {
   // add TILE's base-p digits with carry, then re-chain the partial sums
   // below the highest changed digit.
   __device__ void state_advance(int rl, int d, int dd) {
-    RasrapTileShared &R = *sh;
+    Shared &R = *sh;
     const HaltonDim &h = c_hdim[d];
     const uint32_t p = (uint32_t)h.base;
     const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
@@ -343,23 +344,25 @@ struct GenRasrapRecTile {
       prepare_stateless(rl, base, d, dd);
       return;
     }
-    if (R.st_rl[dd] == rl && R.st_base[dd] + TILE == base) {
-      state_advance(rl, d, dd);
-    } else {
-      state_full(rl, base, d, dd);
-    }
-    R.st_rl[dd] = rl;
-    R.st_base[dd] = base;
-    int N = TILE, J = 0;
-    R.nn[dd][0] = (int16_t)N;
+    if constexpr (PERSIST) {
+      if (R.st_rl[dd] == rl && R.st_base[dd] + TILE == base) {
+        state_advance(rl, d, dd);
+      } else {
+        state_full(rl, base, d, dd);
+      }
+      R.st_rl[dd] = rl;
+      R.st_base[dd] = base;
+      int N = TILE, J = 0;
+      R.nn[dd][0] = (int16_t)N;
 #pragma unroll 1
-    while (N > 1) {
-      N = (int)__umulhi((uint32_t)R.bd[dd][J] + (uint32_t)N - 1u, h.m16) + 1;
-      J++;
-      R.nn[dd][J] = (int16_t)N;
+      while (N > 1) {
+        N = (int)__umulhi((uint32_t)R.bd[dd][J] + (uint32_t)N - 1u, h.m16) + 1;
+        J++;
+        R.nn[dd][J] = (int16_t)N;
+      }
+      R.J[dd] = J;
+      R.sJ[dd] = sh->P[dd][J];
     }
-    R.J[dd] = J;
-    R.sJ[dd] = R.P[dd][J];
   }
   __device__ void prepare_stateless(int rl, uint64_t base, int d, int dd) {
     RasrapTileShared &R = *sh;
@@ -509,6 +512,13 @@ struct GenRasrapCounter {
   }
 };
 
+// u = w 2^-32 + 2^-33 (harness.py:66-67), exactly: the double 1 + u has the
+// mantissa (w << 20) | 2^19, so it is assembled from w with two integer ops
+// and 1 is subtracted exactly (no int->double conversion on the XU pipe).
+__device__ __forceinline__ double philox_u(uint32_t w) {
+  return __hiloint2double((int)(0x3FF00000u | (w >> 12)), (int)((w << 20) | 0x80000u)) - 1.0;
+}
+
 // Philox-4x32-10, counter (b, path_lo, path_hi, 0), u = w 2^-32 + 2^-33
 // (prng.py:180-231, harness.py:53-67).
 struct GenPhilox {
@@ -522,10 +532,10 @@ struct GenPhilox {
     for (int dd = 0; dd < Dc; dd += 4) {  // d0 % 4 == 0
       U4 w = philox4x32_10((uint32_t)((d0 + dd) >> 2), (uint32_t)path, (uint32_t)(path >> 32),
                            0u, k0, k1);
-      zcol[dd * TILE] = (double)w.x * TWO_M32 + TWO_M33;
-      if (dd + 1 < Dc) zcol[(dd + 1) * TILE] = (double)w.y * TWO_M32 + TWO_M33;
-      if (dd + 2 < Dc) zcol[(dd + 2) * TILE] = (double)w.z * TWO_M32 + TWO_M33;
-      if (dd + 3 < Dc) zcol[(dd + 3) * TILE] = (double)w.w * TWO_M32 + TWO_M33;
+      zcol[dd * TILE] = philox_u(w.x);
+      if (dd + 1 < Dc) zcol[(dd + 1) * TILE] = philox_u(w.y);
+      if (dd + 2 < Dc) zcol[(dd + 2) * TILE] = philox_u(w.z);
+      if (dd + 3 < Dc) zcol[(dd + 3) * TILE] = philox_u(w.w);
     }
   }
 };
@@ -621,40 +631,28 @@ struct GenSfc64 {
 // == order of their bit patterns); four inputs are in flight per pass for
 // ILP; the ~9% tail inputs are queued and evaluated 32 at a time.
 // ======================================================================
-__device__ __forceinline__ double invn_fold_i(double p, bool *neg) {
-  const long long HALF = 0x3FE0000000000000LL;   // 0.5
-  const long long TINYB = 0x3CA0000000000000LL;  // 2^-53
-  *neg = __double_as_longlong(p) > HALF;
-  double pl = *neg ? 1.0 - p : p;  // exact for p > 1/2
-  return __double_as_longlong(pl) < TINYB ? InvNormal::TINY : pl;
-}
-__device__ __forceinline__ bool invn_is_tail(double pl) {
-  return __double_as_longlong(pl) < __double_as_longlong(InvNormal::PLOW);
-}
-
 __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc, uint16_t *q) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   int qn = 0;
   for (int d4 = 0; d4 < Dc; d4 += 4) {
-    double pl[4], x[4];
-    bool neg[4], tail[4];
+    double p[4], x[4];
+    bool tail[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       const int dd = d4 + k;
-      double p = dd < Dc ? zt[dd * TILE + threadIdx.x] : 0.5;
-      pl[k] = invn_fold_i(p, &neg[k]);
-      tail[k] = dd < Dc && invn_is_tail(pl[k]);
+      p[k] = dd < Dc ? zt[dd * TILE + threadIdx.x] : 0.5;
+      tail[k] = dd < Dc && invn_tail_p(p[k]);
     }
 #pragma unroll
-    for (int k = 0; k < 4; k++) x[k] = invn_central(pl[k]);
+    for (int k = 0; k < 4; k++) x[k] = invn_central_q(p[k] - 0.5);
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       const int dd = d4 + k;
       const int slot = dd * TILE + threadIdx.x;
       unsigned b = __ballot_sync(0xffffffffu, tail[k]);
       if (tail[k]) q[qn + __popc(b & lt)] = (uint16_t)slot;
-      else if (dd < Dc) zt[slot] = neg[k] ? -x[k] : x[k];
+      else if (dd < Dc) zt[slot] = x[k];
       qn += __popc(b);
     }
   }
@@ -662,7 +660,7 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc, uint16_t *q
   for (int k = lane; k < qn; k += 32) {
     const int slot = q[k];
     bool neg;
-    double pl = invn_fold_i(zt[slot], &neg);
+    double pl = invn_fold(zt[slot], &neg);
     double x = invn_tail(pl);
     zt[slot] = neg ? -x : x;
   }
@@ -772,47 +770,34 @@ struct ModelLibor {
   }
 };
 
-// exp(x) for |x| <= 0.2: Taylor to x^12 (truncation < 2e-19 relative), no
-// range reduction; the MBS shocks xi = sigma_xi * z stay far inside that
-// range (|xi| <= 0.17 at the reference's variance).  Other x: libdevice exp.
-__device__ __forceinline__ double exp_mbs(double x) {
-  if (fabs(x) > 0.2) return exp(x);
-  double p = 2.08767569878681e-09;
-  p = fma(p, x, 2.505210838544172e-08);
-  p = fma(p, x, 2.755731922398589e-07);
-  p = fma(p, x, 2.7557319223985893e-06);
-  p = fma(p, x, 2.48015873015873e-05);
-  p = fma(p, x, 0.0001984126984126984);
-  p = fma(p, x, 0.001388888888888889);
-  p = fma(p, x, 0.008333333333333333);
-  p = fma(p, x, 0.041666666666666664);
-  p = fma(p, x, 0.16666666666666666);
-  p = fma(p, x, 0.5);
-  p = fma(p, x, 1.0);
-  return fma(p, x, 1.0);
-}
-// atan(y) = atan(5/8) + atan(t), t = (y - 5/8)/(1 + 5y/8); for |t| <= 0.2
-// (y in [0.378, 0.943], i.e. MBS rates in [-1.2%, 4.4%]) an odd Taylor
-// series to t^23 (truncation < 2e-19).  Other y: libdevice atan.
+// k0 * exp(sigma_xi * z) as one polynomial in z: the Taylor series of exp
+// to x^9 with x = sigma_xi * z and k0 folded into the coefficients
+// (ModelParams::ecoef, built on the host), valid for |x| <= 0.1 (truncation
+// < 3.1e-17 relative).  The shocks stay there unless |z| > 5 at the
+// reference's variance; beyond that (or for other variances) libdevice exp.
+// atan(y) = atan(c) + atan(t), t = (y - c) / (1 + c y), c = 1/2 below 0.62
+// and 3/4 above: |t| <= 0.1 for y in [0.381, 0.919] (MBS rates -1.2% ..
+// 4.2% at k3 = 10, k4 = 0.5) and the odd series to t^13 is exact to 7e-17;
+// other y: libdevice atan.
 __device__ __forceinline__ double atan_mbs(double y) {
-  const double t = (y - 0.625) * rcp2(fma(0.625, y, 1.0));
-  if (fabs(t) > 0.2) return atan(y);
+  const bool hi = y >= 0.62;
+  const double c = hi ? 0.75 : 0.5;
+  const double t = div2(y - c, fma(c, y, 1.0));
+  if (fabs(t) > 0.1) return atan(y);
   const double t2 = t * t;
-  double p = -0.043478260869565216;
-  p = fma(p, t2, 0.047619047619047616);
-  p = fma(p, t2, -0.05263157894736842);
-  p = fma(p, t2, 0.058823529411764705);
-  p = fma(p, t2, -0.06666666666666667);
-  p = fma(p, t2, 0.07692307692307693);
+  double p = 0.07692307692307693;  // 1/13
   p = fma(p, t2, -0.09090909090909091);
   p = fma(p, t2, 0.1111111111111111);
   p = fma(p, t2, -0.14285714285714285);
   p = fma(p, t2, 0.2);
   p = fma(p, t2, -0.3333333333333333);
-  return fma(t * t2, p, t) + 0.5585993153435624;  // atan(0.625)
+  return fma(t * t2, p, t) + (hi ? 0.6435011087932844 : 0.4636476090008061);
 }
 
-// MBS present value (models.py:430-449), monthly steps.
+// MBS present value (models.py:430-449), monthly steps.  State: discount
+// disc, R = payment * remaining (so the cash flow is one product), the rate
+// and 1 - w of the previous month (1.0 before month 1: R * 1.0 is exact, as
+// the reference's skipped update).
 struct ModelMbs {
   static constexpr bool NORMALS = true;
   static constexpr int MINB = 4;
@@ -820,8 +805,9 @@ struct ModelMbs {
   using Shared = NoShared;
   static __host__ __device__ int gen_dims(int dim) { return dim; }
   const double *ck;
-  double i0, sxi, k0, k1, k2, k3, k4, pay;
-  double disc, rem, rate, prev_w, pv;
+  double i0, sxi, k0, k1, k2, k3, k4, pay, zlim;
+  double ec[MBS_EXP_TERMS];
+  double disc, R, rate, omw, pv;
   __device__ void init(const ModelParams &mp_, Shared &) {
     ck = mp_.table;  // annuity ratios: uniform across the warp, L1-resident
     i0 = mp_.i0;
@@ -832,34 +818,35 @@ struct ModelMbs {
     k3 = mp_.k3;
     k4 = mp_.k4;
     pay = mp_.payment;
+    zlim = mp_.exp_zlim;
+#pragma unroll
+    for (int k = 0; k < MBS_EXP_TERMS; k++) ec[k] = mp_.ecoef[k];
   }
   __device__ void begin() {
     disc = 1.0;
-    rem = 1.0;
+    R = pay;
     rate = i0;
-    prev_w = 0.0;
+    omw = 1.0;
     pv = 0.0;
   }
-  __device__ __forceinline__ void month(int k, double xi) {  // month k+1
-    disc *= rcp2(1.0 + rate);
-    if (k > 0) rem *= 1.0 - prev_w;
-    rate = k0 * exp_mbs(xi) * rate;
-    double w = fma(k2, atan_mbs(fma(k3, rate, k4)), k1);
-    pv = fma(disc * pay * rem, fma(w, __ldg(ck + k), 1.0 - w), pv);
-    prev_w = w;
+  __device__ __forceinline__ double kexp(double z) const {  // k0 * exp(sigma_xi z)
+    if (fabs(z) > zlim) return k0 * exp(sxi * z);
+    double p = ec[MBS_EXP_TERMS - 1];
+#pragma unroll
+    for (int k = MBS_EXP_TERMS - 2; k >= 0; k--) p = fma(p, z, ec[k]);
+    return p;
   }
   // Months in groups of MG: the shocks' exponentials, the discount
   // reciprocals and the prepayment arctangents of a group are independent
   // once the (cheap, serial) rate product is known, so they are issued
-  // together; only disc / rem / pv remain serial.  Same operations and
-  // association as month() (models.py:437-448).
+  // together; only disc / R / pv remain serial (models.py:437-448).
   static constexpr int MG = 4;
   __device__ void chunk(int d0, int Dc, const double *zcol) {
     int kk = 0;
     for (; kk + MG <= Dc; kk += MG) {
       double e[MG], inv[MG], w[MG];
 #pragma unroll
-      for (int m = 0; m < MG; m++) e[m] = k0 * exp_mbs(sxi * zcol[(kk + m) * TILE]);
+      for (int m = 0; m < MG; m++) e[m] = kexp(zcol[(kk + m) * TILE]);
       double r = rate;
 #pragma unroll
       for (int m = 0; m < MG; m++) {
@@ -874,15 +861,21 @@ struct ModelMbs {
       }
 #pragma unroll
       for (int m = 0; m < MG; m++) {
-        const int k = d0 + kk + m;
         disc *= inv[m];
-        if (k > 0) rem *= 1.0 - prev_w;
-        pv = fma(disc * pay * rem, fma(w[m], __ldg(ck + k), 1.0 - w[m]), pv);
-        prev_w = w[m];
+        R *= omw;
+        omw = 1.0 - w[m];
+        pv = fma(disc * R, fma(w[m], __ldg(ck + d0 + kk + m), omw), pv);
       }
       rate = r;
     }
-    for (; kk < Dc; kk++) month(d0 + kk, sxi * zcol[kk * TILE]);
+    for (; kk < Dc; kk++) {
+      disc *= rcp2(1.0 + rate);
+      R *= omw;
+      rate = kexp(zcol[kk * TILE]) * rate;
+      const double w = fma(k2, atan_mbs(fma(k3, rate, k4)), k1);
+      omw = 1.0 - w;
+      pv = fma(disc * R, fma(w, __ldg(ck + d0 + kk), omw), pv);
+    }
   }
   __device__ double payoff() const { return pv; }
 };
