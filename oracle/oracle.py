@@ -20,7 +20,7 @@ HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "build" / "librqmc_oracle.so"
 
 GEN_IDS = {"rasrap-recursive": 0, "rasrap-counter": 1, "philox": 2, "sobol-gray": 3,
-           "sobol-counter": 4, "sfc64": 5}
+           "sobol-counter": 4, "sfc64": 5, "twister": 6, "xorwow": 7}
 MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3}
 FAMILY_IDS = {"twister": 1, "xorwow": 2, "philox": 3, "rasrap": 4, "sobol": 5, "kakutani": 6,
               "sfc64": 7}
@@ -81,6 +81,10 @@ def _declare(L):
     L.orc_run_replications.argtypes = [i32, i32, i32, P(dbl), u64, i64, i64, P(i64), i32,
                                        P(C.c_uint32), i32, P(dbl)]
     L.orc_sfc64_path_uniforms.argtypes = [u64, i64, P(i64), i64, i32, P(dbl)]
+    L.orc_mt19937_init.argtypes = [C.c_void_p, C.c_uint32]
+    L.orc_mt19937_words.argtypes = [C.c_void_p, i64, P(C.c_uint32)]
+    L.orc_xorwow_init.argtypes = [C.c_void_p, u64]
+    L.orc_xorwow_words.argtypes = [C.c_void_p, i64, P(C.c_uint32)]
 
 
 # ---------------------------------------------------------------- seeding
@@ -184,6 +188,32 @@ def sfc64_uniforms(seed: int, m: int, paths, dim: int) -> np.ndarray:
     lib().orc_sfc64_path_uniforms(seed, m, _p(paths, C.c_int64), paths.size, dim,
                                   _p(out, C.c_double))
     return out
+
+
+class _WordStream:
+    """Sequential word generator state owned by Python (prng.py:63-149)."""
+
+    def __init__(self, nbytes: int, init, seed: int, fill):
+        self._buf = C.create_string_buffer(nbytes)
+        self._fill = fill
+        init(self._buf, seed)
+
+    def words(self, n: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.uint32)
+        self._fill(self._buf, n, _p(out, C.c_uint32))
+        return out
+
+
+def mt19937(seed32: int) -> _WordStream:
+    """prng.MT19937(seed) (prng.py:63-72)."""
+    return _WordStream(624 * 4 + 8, lib().orc_mt19937_init, seed32 & 0xFFFFFFFF,
+                       lib().orc_mt19937_words)
+
+
+def xorwow(seed: int) -> _WordStream:
+    """prng.Xorwow(seed) (prng.py:128-134)."""
+    return _WordStream(6 * 4, lib().orc_xorwow_init, seed & 0xFFFFFFFFFFFFFFFF,
+                       lib().orc_xorwow_words)
 
 
 # ---------------------------------------------------------------- models

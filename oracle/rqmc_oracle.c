@@ -659,17 +659,86 @@ void orc_sfc64_path_uniforms(uint64_t seed, int64_t m, const int64_t *paths, int
 }
 
 /* ------------------------------------------------------------------ */
+/* MT19937 and XORWOW word streams (prng.py:40-149)                     */
+/* ------------------------------------------------------------------ */
+
+/* MT19937 with the classic 32-bit seeding (prng.py:63-72); cursor starts at
+ * 624 so the first word triggers a twist (prng.py:43-52). */
+void orc_mt19937_init(orc_mt19937 *g, uint32_t seed) {
+  g->state[0] = seed;
+  for (int i = 1; i < 624; i++) {
+    uint32_t prev = g->state[i - 1];
+    g->state[i] = 1812433253u * (prev ^ (prev >> 30)) + (uint32_t)i;
+  }
+  g->cursor = 624;
+}
+
+/* _mt_fill (prng.py:40-60): in-place twist, then tempering. */
+void orc_mt19937_words(orc_mt19937 *g, int64_t n, uint32_t *out) {
+  uint32_t *st = g->state;
+  for (int64_t i = 0; i < n; i++) {
+    if (g->cursor >= 624) {
+      for (int j = 0; j < 624; j++) {
+        uint32_t y = (st[j] & 0x80000000u) | (st[(j + 1) % 624] & 0x7FFFFFFFu);
+        uint32_t val = st[(j + 397) % 624] ^ (y >> 1);
+        if (y & 1u) val ^= 0x9908B0DFu;
+        st[j] = val;
+      }
+      g->cursor = 0;
+    }
+    uint32_t y = st[g->cursor++];
+    y ^= y >> 11;
+    y ^= (y << 7) & 0x9D2C5680u;
+    y ^= (y << 15) & 0xEFC60000u;
+    y ^= y >> 18;
+    out[i] = y;
+  }
+}
+
+/* Xorwow(seed) (prng.py:128-134): derive_words(seed, 6), re-derived from
+ * seed + 1, + 2, ... while the five xorshift words are all zero. */
+void orc_xorwow_init(orc_xorwow *g, uint64_t seed) {
+  for (;;) {
+    orc_derive_words(seed, 6, g->s);
+    if (g->s[0] | g->s[1] | g->s[2] | g->s[3] | g->s[4]) break;
+    seed = seed + 1;
+  }
+}
+
+/* _xorwow_fill (prng.py:90-115), 32-bit wraparound. */
+void orc_xorwow_words(orc_xorwow *g, int64_t n, uint32_t *out) {
+  uint32_t x = g->s[0], y = g->s[1], z = g->s[2], w = g->s[3], v = g->s[4], d = g->s[5];
+  for (int64_t i = 0; i < n; i++) {
+    uint32_t t = x ^ (x >> 2);
+    x = y;
+    y = z;
+    z = w;
+    w = v;
+    v = (v ^ (v << 4)) ^ (t ^ (t << 1));
+    d += 362437u;
+    out[i] = d + v;
+  }
+  g->s[0] = x;
+  g->s[1] = y;
+  g->s[2] = z;
+  g->s[3] = w;
+  g->s[4] = v;
+  g->s[5] = d;
+}
+
+/* ------------------------------------------------------------------ */
 /* harness.py replication loop                                          */
 /* ------------------------------------------------------------------ */
 
 #define CHUNK_PATHS 8192 /* harness.py:25 */
 
-static const uint64_t FAMILY_ID[6] = {4, 4, 3, 5, 5, 7}; /* seeding.py:17-24; 7 = sfc64 */
+/* seeding.py:17-24 (twister 1, xorwow 2, philox 3, rasrap 4, sobol 5); 7 = sfc64 */
+static const uint64_t FAMILY_ID[8] = {4, 4, 3, 5, 5, 7, 1, 2};
 
 int orc_run_replication(int gen, int model, int dim, const double *mparams, uint64_t seed,
                         int64_t m, const int64_t *grid, int ngrid, const uint32_t *sobol_v,
                         double *theta) {
-  if (gen < 0 || gen > 5 || model < 0 || model > 3 || ngrid < 1) return -1;
+  if (gen < 0 || gen > 7 || model < 0 || model > 3 || ngrid < 1) return -1;
   int64_t nmax = grid[ngrid - 1];
   uint64_t parts[3] = {seed, FAMILY_ID[gen], (uint64_t)m};
   uint64_t key = orc_derive_key(parts, 3); /* harness.py:113 */
@@ -680,6 +749,10 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
   uint32_t *gen_v = NULL, *shift = NULL;
   rasrap_rec rec;
   rasrap_cfg cfg;
+  orc_mt19937 mt;
+  orc_xorwow xw;
+  if (gen == 6) orc_mt19937_init(&mt, (uint32_t)key); /* harness.py:111 key & 0xFFFFFFFF */
+  if (gen == 7) orc_xorwow_init(&xw, key);             /* harness.py:113 */
   if (gen == 0) rec_init(&rec, dim, key);
   if (gen == 1) cfg_make(&cfg, dim, key);
   if (gen == 3 || gen == 4) {
@@ -696,8 +769,11 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
       counter_points(&cfg, idx, cnt, buf);
     } else if (gen == 5) {
       orc_sfc64_path_uniforms(seed, m, idx, cnt, dim, buf);
-    } else if (gen == 2) {
-      orc_philox_words(key, idx, cnt, dim, words);
+    } else if (gen == 2 || gen == 6 || gen == 7) {
+      /* _WordSampler.fill (harness.py:46-50): the next cnt*dim words, row-major */
+      if (gen == 2) orc_philox_words(key, idx, cnt, dim, words);
+      if (gen == 6) orc_mt19937_words(&mt, cnt * dim, words);
+      if (gen == 7) orc_xorwow_words(&xw, cnt * dim, words);
       for (int64_t i = 0; i < cnt * dim; i++)
         buf[i] = (double)words[i] * 2.3283064365386963e-10 + 1.1641532182693481e-10;
     } else {

@@ -87,7 +87,8 @@ double orc_pairwise_sum(const double *a, int64_t n);
 /* One full replication (harness.py:291-315): generator -> model -> prefix
  * estimates theta[g] = np.sum(payoffs[:grid[g]]) / grid[g].
  * gen: 0 rasrap-recursive, 1 rasrap-counter, 2 philox, 3 sobol-gray,
- *      4 sobol-counter, 5 sfc64 (builder-defined per-path streams).  model: 0 libor, 1 mbs, 2 x1, 3 const1.
+ *      4 sobol-counter, 5 sfc64 (builder-defined per-path streams), 6 twister,
+ *      7 xorwow.  model: 0 libor, 1 mbs, 2 x1, 3 const1.
  * mparams: libor {delta, sigma, strike, front_factor, l0[steps]...};
  *          mbs {i0,k0,k1,k2,k3,k4,sigma_xi,payment, ck[months]...}.
  * sobol_v: unscrambled direction words [dim x 32] (gen 3/4 only). */
@@ -99,6 +100,19 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
 int orc_run_replications(int gen, int model, int dim, const double *mparams, uint64_t seed,
                          int64_t first, int64_t count, const int64_t *grid, int ngrid,
                          const uint32_t *sobol_v, int threads, double *theta);
+
+/* MT19937 (prng.py:40-82) and XORWOW (prng.py:90-149) word streams. */
+typedef struct {
+  uint32_t state[624];
+  int cursor;
+} orc_mt19937;
+void orc_mt19937_init(orc_mt19937 *g, uint32_t seed);
+void orc_mt19937_words(orc_mt19937 *g, int64_t n, uint32_t *out);
+typedef struct {
+  uint32_t s[6]; /* x, y, z, w, v, d */
+} orc_xorwow;
+void orc_xorwow_init(orc_xorwow *g, uint64_t seed);
+void orc_xorwow_words(orc_xorwow *g, int64_t n, uint32_t *out);
 
 /* SFC64 (no reference counterpart; numpy.random.SFC64 is the oracle).
  * Per-path stream seeded from derive_words(derive_key(seed, 7, m, path), 6). */

@@ -65,6 +65,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
     ap.add_argument("--out", default=str(HERE))
+    ap.add_argument("--only", default="", help="comma list of sections (e.g. seq)")
     args = ap.parse_args()
     halton, H, M, prng, seeding, sobol = _import_reference(Path(args.ref))
     import numba
@@ -74,6 +75,11 @@ def main():
         {"numpy": np.__version__, "numba": numba.__version__, "scipy": scipy.__version__}
     )
     out = Path(args.out)
+    if args.only:
+        for sec in args.only.split(","):
+            globals()[f"_section_{sec}"](out, versions, H, M, prng, seeding)
+        return
+    _section_seq(out, versions, H, M, prng, seeding)
 
     # ---------------- seeding + randomisation ---------------------------
     fams = sorted(seeding.GENERATOR_IDS.values())
@@ -205,6 +211,57 @@ def main():
     tz["stride_philox_theta"] = rep.estimates("philox", 5000)
     np.savez_compressed(out / "theta.npz", **tz)
     print("golden fixtures written to", out)
+
+
+def _section_seq(out, versions, H, M, prng, seeding):
+    """MT19937 / XORWOW word streams and replication estimates (prng.py:40-149,
+    harness.py:37-50, 99-125)."""
+    z = {"versions": versions}
+    mt_seeds = np.array([0, 1, 5489, 2**32 - 1, 20120224], dtype=np.uint64)
+    xw_seeds = np.array([0, 1, 123456789, 2**64 - 1, 20120224], dtype=np.uint64)
+    z["mt_seeds"] = mt_seeds
+    z["mt_words"] = np.stack([_words(prng.MT19937(int(s)), 5000) for s in mt_seeds])
+    z["xw_seeds"] = xw_seeds
+    z["xw_words"] = np.stack([_words(prng.Xorwow(int(s)), 5000) for s in xw_seeds])
+    # far into a stream: rows of the harness samplers (chunked fill)
+    for gen, dim, m, nmax in (("twister", 20, 1, 2**20 + 1024), ("xorwow", 20, 1, 2**20 + 1024),
+                              ("twister", 80, 2, 50000), ("xorwow", 360, 3, 20000),
+                              ("twister", 360, 1, 20000)):
+        tag = f"{gen}_d{dim}_m{m}"
+        rows = _rows(nmax, head=300, step=7919)
+        z[f"{tag}_rows"] = rows
+        z[f"{tag}_points"] = _fill_rows(H.make_sampler(gen, dim, SEED, m), dim, nmax, rows)
+    np.savez_compressed(out / "prng_seq.npz", **z)
+
+    tz = {"versions": versions}
+    s20 = M.LiborModel(M.LiborConfig(maturity=5.0, accrual=0.25))
+    s80 = M.LiborModel(M.LiborConfig(maturity=20.0, accrual=0.25))
+    runs = [
+        ("libor20_twister", "libor", "twister", (1000, 8192, 20_000), 8, s20),
+        ("libor20_xorwow", "libor", "xorwow", (1000, 8192, 20_000), 8, s20),
+        ("libor80_twister", "libor", "twister", (2048,), 4, s80),
+        ("libor80_xorwow", "libor", "xorwow", (2048,), 4, s80),
+        ("mbs_twister", "mbs", "twister", (500, 3000), 4, M.MbsModel()),
+        ("mbs_xorwow", "mbs", "xorwow", (3000,), 4, M.MbsModel()),
+        ("x1_twister", "x1", "twister", (7, 1000, 65_536), 4, M.FirstCoordinateModel()),
+        ("x1_xorwow", "x1", "xorwow", (129, 65_536), 4, M.FirstCoordinateModel()),
+    ]
+    for tag, mname, gen, grid, reps, model in runs:
+        cfg = H.ExperimentConfig(model=mname, generator=gen, n_grid=grid, replications=reps,
+                                 seed=SEED, workers=4)
+        rep = H.run_experiment(cfg, model=model)
+        tz[f"{tag}_grid"] = np.array(grid, dtype=np.int64)
+        tz[f"{tag}_theta"] = np.stack([rep.estimates(gen, n) for n in grid])  # [grid, M]
+        tz[f"{tag}_mean"] = np.array([rep.row(gen, n).mean for n in grid])
+        tz[f"{tag}_std"] = np.array([rep.row(gen, n).std for n in grid])
+        print(tag, tz[f"{tag}_mean"], flush=True)
+    np.savez_compressed(out / "theta_seq.npz", **tz)
+
+
+def _words(gen, n: int) -> np.ndarray:
+    w = np.empty(n, dtype=np.uint32)
+    gen.fill_words(w)
+    return w
 
 
 if __name__ == "__main__":

@@ -222,3 +222,62 @@ def test_sfc64_matches_numpy(oracle):
         bg.random_raw(12)
         expect = np.random.Generator(bg).random(37)
         assert np.array_equal(mine[r], expect)
+
+
+# ---------------------------------------------------------------- MT19937 / XORWOW
+def test_mt19937_words(oracle, golden):
+    g = golden("prng_seq")
+    for s, w in zip(g["mt_seeds"], g["mt_words"]):
+        assert np.array_equal(oracle.mt19937(int(s)).words(len(w)), w)
+
+
+def test_mt19937_kat(oracle):
+    # test_prng.py:43-53: 10000th output of the classic 5489 seeding
+    assert oracle.mt19937(5489).words(10000)[-1] == 4123659995
+    # numpy's legacy RandomState seeding is the same init_genrand recursion
+    rs = np.random.RandomState(20120224)
+    assert np.array_equal(oracle.mt19937(20120224).words(2000),
+                          rs.randint(0, 2**32, size=2000, dtype=np.uint64).astype(np.uint32))
+
+
+def test_xorwow_words(oracle, golden):
+    g = golden("prng_seq")
+    for s, w in zip(g["xw_seeds"], g["xw_words"]):
+        assert np.array_equal(oracle.xorwow(int(s)).words(len(w)), w)
+
+
+def test_xorwow_matches_independent_recurrence(oracle):
+    # test_prng.py:28-39 style: Marsaglia's recurrence written out in Python ints
+    st = [int(x) for x in oracle.derive_words(987654321, 6)]
+    x, y, z, w, v, d = st
+    ref = []
+    for _ in range(500):
+        t = (x ^ (x >> 2)) & 0xFFFFFFFF
+        x, y, z, w = y, z, w, v
+        v = (v ^ ((v << 4) & 0xFFFFFFFF)) ^ (t ^ ((t << 1) & 0xFFFFFFFF))
+        d = (d + 362437) & 0xFFFFFFFF
+        ref.append((d + v) & 0xFFFFFFFF)
+    assert list(oracle.xorwow(987654321).words(500)) == ref
+
+
+THETA_SEQ_RUNS = {
+    "libor20_twister": ("twister", "s20"),
+    "libor20_xorwow": ("xorwow", "s20"),
+    "libor80_twister": ("twister", "s80"),
+    "libor80_xorwow": ("xorwow", "s80"),
+    "mbs_twister": ("twister", "mbs"),
+    "mbs_xorwow": ("xorwow", "mbs"),
+    "x1_twister": ("twister", "x1"),
+    "x1_xorwow": ("xorwow", "x1"),
+}
+
+
+@pytest.mark.parametrize("tag", sorted(THETA_SEQ_RUNS))
+def test_sequential_prng_estimates_bit_exact(oracle, golden, tag):
+    gen, mk = THETA_SEQ_RUNS[tag]
+    model = _golden_models(golden)[mk]
+    t = golden("theta_seq")
+    theta = t[f"{tag}_theta"]
+    mine = oracle.run_replications(gen, model, SEED, 1, theta.shape[1], t[f"{tag}_grid"],
+                                   threads=4)
+    assert np.array_equal(mine.T, theta)
