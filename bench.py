@@ -132,7 +132,7 @@ def device_step(gen_id, model, seed, first, count, grid, theta, lib, C, _lib):
     n = C.c_int32(0)
     _lib.check(lib.rq_estimate(h, C.byref(ms), g.ctypes.data_as(C.POINTER(C.c_int64)), g.size,
                                theta.data_ptr(), C.byref(n), st))
-    return h, n.value + (1 if gen_id in (0, 1, 3, 4) else 0), keep
+    return h, n.value + (1 if gen_id in (0, 1, 3, 4, 7) else 0), keep  # + setup kernel
 
 
 def run_stream(args) -> dict:

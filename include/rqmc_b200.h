@@ -41,7 +41,9 @@ enum rq_generator {
   RQ_GEN_PHILOX = 2,           /* harness._PhiloxSampler  harness.py:53-72  */
   RQ_GEN_SOBOL_GRAY = 3,       /* sobol.SobolGray         sobol.py:330-346  */
   RQ_GEN_SOBOL_COUNTER = 4,    /* sobol.SobolCounter      sobol.py:349-372  */
-  RQ_GEN_SFC64 = 5             /* per-path SFC64 streams (numpy SFC64 core) */
+  RQ_GEN_SFC64 = 5,            /* per-path SFC64 streams (numpy SFC64 core) */
+  RQ_GEN_TWISTER = 6,          /* prng.MT19937 word stream  prng.py:40-82, harness.py:110-111 */
+  RQ_GEN_XORWOW = 7            /* prng.Xorwow word stream   prng.py:90-149, harness.py:112-113 */
 };
 
 /* Model kinds: models.LiborModel (models.py:296-329), models.MbsModel
@@ -84,7 +86,9 @@ void rq_sampler_destroy(rq_sampler *s);
  * out_dev[count][dim] row-major float64. */
 int rq_sampler_points(rq_sampler *s, int32_t rep_local, int64_t first, int64_t count,
                       double *out_dev, void *stream);
-/* sampler.at(indices) (halton.py:507, sobol.py:359, harness.py:69) */
+/* sampler.at(indices) (halton.py:507, sobol.py:359, harness.py:69).  The
+ * sequential word streams (twister, xorwow) have no at() in the reference
+ * (_WordSampler, harness.py:37-50): RQ_ERR_VALUE. */
 int rq_sampler_points_at(rq_sampler *s, int32_t rep_local, const int64_t *idx_dev,
                          int64_t count, double *out_dev, void *stream);
 /* Rasrap tables of one replication, for inspection/tests (strides padded

@@ -27,6 +27,8 @@ GEN_IDS = {
     "sobol-gray": 3,
     "sobol-counter": 4,
     "sfc64": 5,
+    "twister": 6,
+    "xorwow": 7,
 }
 MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3}
 

@@ -152,6 +152,38 @@ const HostTables &host_tables() {
   return T;
 }
 
+// Columns of the XORWOW xorshift transition A (prng.py:97-108) on the
+// 160-bit state (x, y, z, w, v), and of A^(2^k) by repeated squaring:
+// cols[k][c] = A^(2^k) e_c, padded to XW_COLW words.
+std::vector<uint32_t> xorwow_jump_columns() {
+  const int W = rq::XW_COLW;
+  std::vector<uint32_t> cols((size_t)rq::XW_JUMPS * 160 * W, 0u);
+  auto apply = [&](const uint32_t *M, const uint32_t *v, uint32_t *o) {
+    uint32_t r[5] = {0, 0, 0, 0, 0};
+    for (int c = 0; c < 160; c++)
+      if ((v[c / 32] >> (c % 32)) & 1u)
+        for (int i = 0; i < 5; i++) r[i] ^= M[c * W + i];
+    for (int i = 0; i < 5; i++) o[i] = r[i];
+  };
+  for (int c = 0; c < 160; c++) {
+    uint32_t e[5] = {0, 0, 0, 0, 0};
+    e[c / 32] = 1u << (c % 32);
+    const uint32_t x = e[0], t = x ^ (x >> 2), v = e[4];
+    uint32_t *o = &cols[c * W];
+    o[0] = e[1];
+    o[1] = e[2];
+    o[2] = e[3];
+    o[3] = e[4];
+    o[4] = (v ^ (v << 4)) ^ (t ^ (t << 1));
+  }
+  for (int k = 1; k < rq::XW_JUMPS; k++) {
+    const uint32_t *M = &cols[(size_t)(k - 1) * 160 * W];
+    uint32_t *N = &cols[(size_t)k * 160 * W];
+    for (int c = 0; c < 160; c++) apply(M, M + c * W, N + c * W);
+  }
+  return cols;
+}
+
 int ensure_device_tables() {
   static std::mutex mu;
   static std::vector<int> done;
@@ -168,6 +200,8 @@ int ensure_device_tables() {
   const HostTables &T = host_tables();
   RQ_CUDA(rq::upload_halton_dims(T.dims.data(), (int)T.dims.size(), T.wts.data(),
                                  T.cscale.data(), (int)T.wts.size()));
+  static const std::vector<uint32_t> xw = xorwow_jump_columns();
+  RQ_CUDA(rq::upload_xorwow_jumps(xw.data(), xw.size()));
   done.push_back(dev);
   return RQ_OK;
 }
@@ -347,7 +381,7 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
                       int64_t rep_first, int32_t rep_count, void *stream) {
   if (!out) return fail(RQ_ERR_VALUE, "out is NULL");
   *out = nullptr;
-  if (generator < 0 || generator > rq::GEN_SFC64)
+  if (generator < 0 || generator > rq::GEN_LAST)
     return fail(RQ_ERR_VALUE, "unknown generator id %d", generator);
   if (dim < 1) return fail(RQ_ERR_VALUE, "dimension must be >= 1");
   if (rep_count < 1) return fail(RQ_ERR_VALUE, "rep_count must be >= 1");
@@ -436,8 +470,72 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
     }
     t.sobol_v = gen;
     t.sobol_shift = sh;
+  } else if (generator == rq::GEN_XORWOW) {
+    cudaError_t e = cudaMallocAsync(&S->mem, sizeof(uint32_t) * 6 * rep_count, s);
+    if (e == cudaSuccess) {
+      KTimer kt(&g_stats.setup_ms, s);
+      e = rq::launch_xorwow_setup(t, (uint32_t *)S->mem, s);
+    }
+    if (e != cudaSuccess) {
+      if (S->mem) cudaFreeAsync(S->mem, s);
+      delete S;
+      return fail(RQ_ERR_CUDA, "xorwow setup: %s", cudaGetErrorString(e));
+    }
+    t.xw_state = (const uint32_t *)S->mem;
   }
   *out = S;
+  return RQ_OK;
+}
+
+// Sequential streams: segment layout, MT19937 snapshots and the per-CTA
+// word scratch for paths [p0, p0 + nmax) of batches of <= B replications.
+// The snapshot walk is sequential per replication (latency bound), so it is
+// launched for a whole group of batches at once (<= 256 MiB of snapshots).
+struct SeqRun {
+  rq::SeqArgs q{};
+  int ctas = 0;
+  int64_t grp0 = 0, grpn = 0, grp_cap = 0;
+  uint32_t *snap = nullptr;
+  void *mem = nullptr;
+  cudaStream_t stream = nullptr;  // the work stream: freed in stream order
+  ~SeqRun() {
+    if (mem) cudaFreeAsync(mem, stream);
+  }
+};
+static int seq_begin(const rq::RepTables &t, const rq::ModelParams &mp, int B, int64_t p0,
+                     int64_t nmax, SeqRun &R, cudaStream_t s) {
+  int64_t L;
+  int segs;
+  rq::seq_layout(t, mp, B, nmax, &L, &segs, &R.ctas);
+  R.q.p0 = p0;
+  R.q.seg_len = L;
+  R.q.segs_per_rep = segs;
+  if (t.gen != rq::GEN_TWISTER) return RQ_OK;
+  const size_t per_rep = sizeof(uint32_t) * rq::MT_N * (size_t)segs;
+  int64_t G = std::max<int64_t>(B, ((int64_t)256 << 20) / (int64_t)per_rep / B * B);
+  G = std::min<int64_t>(G, t.rep_count);
+  R.grp_cap = G;
+  size_t b_scr = sizeof(uint32_t) * (size_t)R.ctas * t.dim * 128;
+  RQ_CUDA(cudaMallocAsync(&R.mem, per_rep * G + b_scr, s));
+  R.stream = s;
+  R.snap = (uint32_t *)R.mem;
+  R.q.scratch = R.snap + (size_t)rq::MT_N * segs * G;
+  R.grpn = 0;
+  return RQ_OK;
+}
+// position the run on local replications [r0, r0 + rn): snapshots + grid
+static int seq_batch(const rq::RepTables &t, int r0, int rn, SeqRun &R, int *blocks,
+                     int *launched, cudaStream_t s) {
+  *blocks = (int)std::min<int64_t>((int64_t)rn * R.q.segs_per_rep, R.ctas);
+  if (t.gen != rq::GEN_TWISTER) return RQ_OK;
+  if (r0 < R.grp0 || r0 + rn > R.grp0 + R.grpn) {
+    R.grp0 = r0;
+    R.grpn = std::min<int64_t>(R.grp_cap, t.rep_count - r0);
+    KTimer kt(&g_stats.setup_ms, s);
+    RQ_CUDA(rq::launch_mt_snap(t, r0, (int)R.grpn, R.q, R.snap, s));
+    if (launched) *launched += 1;
+  }
+  R.q.mt_snap = R.snap + (size_t)rq::MT_N * R.q.segs_per_rep * (r0 - R.grp0);
   return RQ_OK;
 }
 
@@ -462,7 +560,19 @@ int rq_sampler_points(rq_sampler *s, int32_t rep_local, int64_t first, int64_t c
   if (first + count > (int64_t)1 << 32)
     return fail(RQ_ERR_RANGE, "point index %lld exceeds 2^32", (long long)(first + count));
   if (count == 0) return RQ_OK;
-  RQ_CUDA(rq::launch_points(s->t, rep_local, first, nullptr, count, out_dev, (cudaStream_t)stream));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rq::gen_sequential(s->t.gen)) {  // _WordSampler.fill: words from the cursor on
+    rq::ModelParams mp{};
+    mp.kind = rq::MODEL_POINTS;
+    mp.dim = s->t.dim;
+    SeqRun R;
+    int blocks = 0;
+    if ((rc = seq_begin(s->t, mp, 1, first, count, R, st))) return rc;
+    if ((rc = seq_batch(s->t, rep_local, 1, R, &blocks, nullptr, st))) return rc;
+    RQ_CUDA(rq::launch_paths_seq(s->t, mp, rep_local, 1, count, R.q, blocks, out_dev, nullptr, st));
+    return RQ_OK;
+  }
+  RQ_CUDA(rq::launch_points(s->t, rep_local, first, nullptr, count, out_dev, st));
   return RQ_OK;
 }
 
@@ -471,6 +581,8 @@ int rq_sampler_points_at(rq_sampler *s, int32_t rep_local, const int64_t *idx_de
   int rc = check_rep(s, rep_local);
   if (rc) return rc;
   if (count <= 0) return count < 0 ? fail(RQ_ERR_VALUE, "count < 0") : RQ_OK;
+  if (rq::gen_sequential(s->t.gen))  // harness._WordSampler has no at() (harness.py:37-50)
+    return fail(RQ_ERR_VALUE, "sequential word streams have no counter-based at()");
   RQ_CUDA(rq::launch_points(s->t, rep_local, 0, idx_dev, count, out_dev, (cudaStream_t)stream));
   return RQ_OK;
 }
@@ -573,10 +685,19 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
   RQ_CUDA(cudaMallocAsync((void **)&tickets, sizeof(unsigned) * B, st));
   RQ_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * B, st));
   int launched = 0;
+  SeqRun R;
+  if (rq::gen_sequential(s->t.gen) && (rc = seq_begin(s->t, mp, (int)B, 0, nmax, R, st)))
+    return rc;
   for (int64_t r0 = 0; r0 < s->t.rep_count; r0 += B) {
     int rn = (int)std::min<int64_t>(B, s->t.rep_count - r0);
     cudaError_t e;
-    {
+    if (rq::gen_sequential(s->t.gen)) {
+      int blocks = 0;
+      if ((rc = seq_batch(s->t, (int)r0, rn, R, &blocks, &launched, st))) return rc;
+      KTimer kt(&g_stats.paths_ms, st);
+      e = rq::launch_paths_seq(s->t, mp, (int)r0, rn, nmax, R.q, blocks, pay, &launched, st);
+      g_stats.paths_launches++;
+    } else {
       KTimer kt(&g_stats.paths_ms, st);
       e = rq::launch_paths(s->t, mp, (int)r0, rn, nmax, pay, &launched, st);
       g_stats.paths_launches++;
@@ -617,8 +738,9 @@ int rq_run_replications(int generator, const rq_model *model, uint64_t seed, int
     rq_sampler *S = nullptr;
     if ((rc = rq_sampler_create(&S, generator, model ? model->dim : 0, seed, rep_first + r0, rn, st)))
       return rc;
-    if (kernel_launches && generator != rq::GEN_PHILOX && generator != rq::GEN_SFC64)
-      *kernel_launches += 1;
+    if (kernel_launches && generator != rq::GEN_PHILOX && generator != rq::GEN_SFC64 &&
+        generator != rq::GEN_TWISTER)
+      *kernel_launches += 1;  // the randomisation setup kernel
     rc = rq_estimate(S, model, grid_host, ngrid, theta_dev + r0 * ngrid, kernel_launches, st);
     RQ_CUDA(cudaStreamSynchronize(st));
     rq_sampler_destroy(S);
@@ -661,6 +783,8 @@ int rq_stream_normals(rq_sampler *s, int32_t rep_local, int64_t npoints, double 
   int rc = check_rep(s, rep_local);
   if (rc) return rc;
   if (npoints < 1 || npoints > ((int64_t)1 << 32)) return fail(RQ_ERR_VALUE, "npoints outside 1..2^32");
+  if (rq::gen_sequential(s->t.gen))
+    return fail(RQ_ERR_VALUE, "the normals stream is for counter/QMC generators (config 4)");
   cudaStream_t st = (cudaStream_t)stream;
   int blocks = rq::paths_grid_blocks(s->t, rq::ModelParams{rq::MODEL_X1, s->t.dim});
   double *bs = nullptr;

@@ -19,8 +19,23 @@ enum Gen : int {
   GEN_SOBOL_GRAY = 3,
   GEN_SOBOL_COUNTER = 4,
   GEN_SFC64 = 5,
+  GEN_TWISTER = 6,  // MT19937 word stream (prng.py:40-82), one per replication
+  GEN_XORWOW = 7,   // XORWOW word stream (prng.py:90-149), one per replication
 };
-enum ModelKind : int { MODEL_LIBOR = 0, MODEL_MBS = 1, MODEL_X1 = 2, MODEL_CONST1 = 3 };
+constexpr int GEN_LAST = GEN_XORWOW;
+__host__ __device__ constexpr bool gen_sequential(int g) {
+  return g == GEN_TWISTER || g == GEN_XORWOW;
+}
+constexpr int MT_N = 624;       // MT19937 state words
+constexpr int XW_JUMPS = 48;    // XORWOW jump matrices A^(2^k), k < XW_JUMPS
+constexpr int XW_COLW = 8;      // words per matrix column (5 used, padded for 128-bit loads)
+enum ModelKind : int {
+  MODEL_LIBOR = 0,
+  MODEL_MBS = 1,
+  MODEL_X1 = 2,
+  MODEL_CONST1 = 3,
+  MODEL_POINTS = 4,  // internal: write the uniforms (sampler.fill of a sequential stream)
+};
 
 // Per-dimension Halton constants (depend only on the d-th prime).  Offsets
 // are prefix sums over dimensions 0..d-1, identical for every replication.
@@ -57,6 +72,23 @@ struct RepTables {
   // Sobol
   const uint32_t *sobol_v;     // [rep][dim][32] scrambled direction words
   const uint32_t *sobol_shift; // [rep][dim]
+  // XORWOW: per-replication initial state (x, y, z, w, v, d) (prng.py:128-134)
+  const uint32_t *xw_state;    // [rep][6]
+};
+
+// Segments of the sequential word streams (MT19937 / XORWOW).  A
+// replication's paths [p0, p0 + nmax) are cut into segments of seg_len paths;
+// a segment is one unit of work for one CTA.  MT19937: the CTA shares one
+// generator state, loaded from a snapshot taken by k_mt_snap at the
+// segment's first word; XORWOW: every thread owns a run of consecutive
+// paths and jumps its own state there with precomputed matrix powers.
+struct SeqArgs {
+  int64_t p0;          // first path of the range (sampler.fill cursor; 0 for estimates)
+  int64_t seg_len;     // paths per segment (multiple of the tile)
+  int32_t segs_per_rep;
+  const uint32_t *mt_snap;  // [rep - rep_local0][seg][MT_N] raw MT state after the twist that
+                            // produced the segment's first word
+  uint32_t *scratch;        // [gridDim][dim][TILE] tempered MT words of a tile
 };
 
 struct ModelParams {
@@ -94,6 +126,16 @@ cudaError_t launch_points(const RepTables &t, int rep_local, int64_t first,
 cudaError_t launch_paths(const RepTables &t, const ModelParams &mp, int rep_local0,
                          int rep_n, int64_t nmax, double *payoffs, int *launched,
                          cudaStream_t s);
+cudaError_t upload_xorwow_jumps(const uint32_t *cols, size_t words);
+cudaError_t launch_xorwow_setup(const RepTables &t, uint32_t *state, cudaStream_t s);
+// choose the segment length / grid of the sequential-stream path kernel
+void seq_layout(const RepTables &t, const ModelParams &mp, int rep_n, int64_t nmax,
+                int64_t *seg_len, int *segs_per_rep, int *blocks);
+cudaError_t launch_mt_snap(const RepTables &t, int rep_local0, int rep_n, const SeqArgs &q,
+                           uint32_t *snap, cudaStream_t s);
+cudaError_t launch_paths_seq(const RepTables &t, const ModelParams &mp, int rep_local0,
+                             int rep_n, int64_t nmax, const SeqArgs &q, int blocks,
+                             double *payoffs, int *launched, cudaStream_t s);
 cudaError_t launch_reduce(const SumPlan &plan, const double *payoffs, int64_t pay_stride,
                           int reps, double *theta, int theta_stride, double *scratch,
                           unsigned *tickets, cudaStream_t s);

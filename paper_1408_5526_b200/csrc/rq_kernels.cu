@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <type_traits>
 
 #include "rq_device.cuh"
@@ -626,6 +627,234 @@ struct GenSfc64 {
 };
 
 // ======================================================================
+// Sequential word streams (prng.py:40-149).  The reference consumes one
+// stream per replication row-major: coordinate d of path i is word
+// i * dim + d, u = w 2^-32 + 2^-33 (harness.py:46-50).  Both generators
+// work on segments of a replication (SeqArgs): begin_segment() positions
+// the stream, unit() yields the uniforms of the thread's current path.
+// ======================================================================
+constexpr uint32_t XW_WEYL = 362437u;
+__device__ uint32_t g_xw_jump[XW_JUMPS * 160 * XW_COLW];  // columns of A^(2^k)
+
+cudaError_t upload_xorwow_jumps(const uint32_t *cols, size_t words) {
+  if (words != (size_t)XW_JUMPS * 160 * XW_COLW) return cudaErrorInvalidValue;
+  return cudaMemcpyToSymbol(g_xw_jump, cols, sizeof(uint32_t) * words);
+}
+
+// Xorwow(key) (prng.py:128-134): derive_words(key, 6), key + 1, ... while
+// the xorshift words are all zero.  One thread per replication.
+__global__ void k_xorwow_setup(RepTables t, uint32_t *state) {
+  const int rl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rl >= t.rep_count) return;
+  uint64_t key = derive_key3(t.seed, 2, (uint64_t)(t.rep_first + rl));  // family "xorwow"
+  uint32_t w[6];
+  for (;;) {
+    const uint64_t z1 = splitmix64(key), z2 = splitmix64(z1), z3 = splitmix64(z2);
+    w[0] = (uint32_t)z1;
+    w[1] = (uint32_t)(z1 >> 32);
+    w[2] = (uint32_t)z2;
+    w[3] = (uint32_t)(z2 >> 32);
+    w[4] = (uint32_t)z3;
+    w[5] = (uint32_t)(z3 >> 32);
+    if (w[0] | w[1] | w[2] | w[3] | w[4]) break;
+    key += 1;
+  }
+  for (int k = 0; k < 6; k++) state[rl * 6 + k] = w[k];
+}
+
+// XORWOW, one stream per replication: thread t of a segment owns the run of
+// paths [t * ntile, (t + 1) * ntile) and generates its words in order; the
+// state is jumped to the run's first word W by the GF(2) matrices A^(2^k)
+// of the xorshift part for the set bits of W (the Weyl counter d advances
+// by 362437 W).
+struct GenXorwow {
+  static constexpr bool RUNS = true;
+  using Shared = NoShared;
+  const RepTables *t;
+  uint32_t x, y, z, w, v, d;
+  __device__ void setup(const RepTables &t_, Shared &, uint32_t *) { t = &t_; }
+  __device__ void begin_segment(int rl, int, int, int64_t, int64_t my_first_path, int dim) {
+    const uint32_t *s0 = t->xw_state + rl * 6;
+    uint32_t s[5] = {s0[0], s0[1], s0[2], s0[3], s0[4]};
+    const uint64_t W = (uint64_t)my_first_path * (uint64_t)dim;
+    d = s0[5] + XW_WEYL * (uint32_t)W;
+#pragma unroll 1
+    for (int k = 0; k < XW_JUMPS; k++) {
+      if (!((W >> k) & 1u)) continue;
+      const uint4 *col = reinterpret_cast<const uint4 *>(g_xw_jump + (size_t)k * 160 * XW_COLW);
+      uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0, o4 = 0;
+#pragma unroll
+      for (int wd = 0; wd < 5; wd++) {
+        const uint32_t bits = s[wd];
+#pragma unroll 4
+        for (int b = 0; b < 32; b++) {
+          const uint4 c = __ldg(col + 2 * (wd * 32 + b));
+          const uint32_t c4 = __ldg(reinterpret_cast<const uint32_t *>(col + 2 * (wd * 32 + b) + 1));
+          const uint32_t m = 0u - ((bits >> b) & 1u);
+          o0 ^= c.x & m;
+          o1 ^= c.y & m;
+          o2 ^= c.z & m;
+          o3 ^= c.w & m;
+          o4 ^= c4 & m;
+        }
+      }
+      s[0] = o0;
+      s[1] = o1;
+      s[2] = o2;
+      s[3] = o3;
+      s[4] = o4;
+    }
+    x = s[0];
+    y = s[1];
+    z = s[2];
+    w = s[3];
+    v = s[4];
+  }
+  __device__ __forceinline__ uint32_t next() {  // _xorwow_fill (prng.py:97-110)
+    const uint32_t tt = x ^ (x >> 2);
+    x = y;
+    y = z;
+    z = w;
+    w = v;
+    v = (v ^ (v << 4)) ^ (tt ^ (tt << 1));
+    d += XW_WEYL;
+    return d + v;
+  }
+  __device__ void unit(int, int, int, int Dc, double *zt) {
+    for (int dd = 0; dd < Dc; dd++) zt[dd * TILE + threadIdx.x] = philox_u(next());
+  }
+  // words of the path the model does not read (f = x_1 reads one of dim)
+  __device__ void skip(int n) {
+    for (int k = 0; k < n; k++) next();
+  }
+};
+
+// MT19937 twist of a whole state block (prng.py:44-51) from `o` into `n`.
+// In the reference's in-place loop word j reads o[j], o[j+1] and the word
+// at j+397 (mod 624), which is already new for j >= 227.  Following the
+// chain j -> j+227 -> j+454 every new word is a function of old words and
+// of its own chain's previous link (j = 623 also needs n[0], recomputed by
+// that thread from old words), so thread k < 227 produces n[k], n[k+227]
+// and n[k+454] with no exchange and the twist costs one CTA barrier.
+__device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t c) {
+  const uint32_t yy = (a & 0x80000000u) | (b & 0x7FFFFFFFu);
+  return c ^ (yy >> 1) ^ ((yy & 1u) ? 0x9908B0DFu : 0u);
+}
+__device__ void mt_twist(const uint32_t *o, uint32_t *n) {
+  for (int k = threadIdx.x; k < 227; k += blockDim.x) {
+    const uint32_t a = mt_mix(o[k], o[k + 1], o[k + 397]);
+    const uint32_t b = mt_mix(o[k + 227], o[k + 228], a);
+    n[k] = a;
+    n[k + 227] = b;
+    if (k < MT_N - 454) {
+      const uint32_t nxt = k == MT_N - 455 ? mt_mix(o[0], o[1], o[397]) : o[k + 455];
+      n[k + 454] = mt_mix(o[k + 454], nxt, b);
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ uint32_t mt_temper(uint32_t yv) {
+  yv ^= yv >> 11;
+  yv ^= (yv << 7) & 0x9D2C5680u;
+  yv ^= (yv << 15) & 0xEFC60000u;
+  return yv ^ (yv >> 18);
+}
+
+// Snapshots for the segments of replications rep_local0.. (one CTA each):
+// MT19937(key & 0xFFFFFFFF) (prng.py:66-72), twisted in order; the state
+// after the twist that yields word W_s = (p0 + s seg_len) dim is stored for
+// every segment s (word W_s is then at position W_s mod 624).
+__global__ void __launch_bounds__(256) k_mt_snap(RepTables t, int rep_local0, int dim,
+                                                 SeqArgs q, uint32_t *snap) {
+  __shared__ uint32_t st[2][MT_N];
+  const int rl = rep_local0 + blockIdx.x;
+  if (threadIdx.x == 0) {
+    uint32_t prev = (uint32_t)derive_key3(t.seed, 1, (uint64_t)(t.rep_first + rl));
+    st[0][0] = prev;
+    for (int i = 1; i < MT_N; i++) {
+      prev = 1812433253u * (prev ^ (prev >> 30)) + (uint32_t)i;
+      st[0][i] = prev;
+    }
+  }
+  __syncthreads();
+  int cur = 0;
+  int64_t twists = 0;  // twists applied so far
+  for (int sg = 0; sg < q.segs_per_rep; sg++) {
+    const int64_t W = (q.p0 + (int64_t)sg * q.seg_len) * dim;
+    const int64_t need = W / MT_N + 1;
+    for (; twists < need; twists++) {
+      mt_twist(st[cur], st[cur ^ 1]);
+      cur ^= 1;
+    }
+    uint32_t *dst = snap + ((int64_t)blockIdx.x * q.segs_per_rep + sg) * MT_N;
+    for (int j = threadIdx.x; j < MT_N; j += blockDim.x) dst[j] = st[cur][j];
+  }
+}
+
+// MT19937, one stream per replication, CTA-cooperative: the CTA owns a
+// segment, loads its snapshot and, for every tile of TILE consecutive
+// paths, twists and tempers the tile's words (path-major) into a per-CTA
+// scratch laid out [dim][TILE], from which every thread reads its path.
+struct GenTwister {
+  static constexpr bool RUNS = false;
+  struct Shared {
+    uint32_t st[2][MT_N];
+  };
+  const RepTables *t;
+  Shared *sh;
+  uint32_t *scr;  // this CTA's [dim][TILE]
+  const SeqArgs *q;
+  int cur, pos;   // current state buffer, next word's position in it
+  uint32_t dim_m; // ceil(2^32 / dim): k / dim for k < 2^32 / dim
+  int dim;
+  __device__ void setup(const RepTables &t_, Shared &s, uint32_t *scratch) {
+    t = &t_;
+    sh = &s;
+    scr = scratch;
+  }
+  __device__ void set_seq(const SeqArgs &q_, int dim_) {
+    q = &q_;
+    dim = dim_;
+    dim_m = (uint32_t)((((uint64_t)1 << 32) + dim_ - 1) / dim_);
+  }
+  __device__ void begin_segment(int, int rb, int sg, int64_t seg_first_path, int64_t, int) {
+    const uint32_t *src = q->mt_snap + ((int64_t)rb * q->segs_per_rep + sg) * MT_N;
+    __syncthreads();  // previous segment's readers are done with the state
+    for (int j = threadIdx.x; j < MT_N; j += blockDim.x) sh->st[0][j] = src[j];
+    cur = 0;
+    pos = (int)((seg_first_path * dim) % MT_N);
+    __syncthreads();
+  }
+  // words of tile paths [0, npaths) -> scratch (all threads; CTA barriers)
+  __device__ void fill_tile(int npaths) {
+    const uint32_t total = (uint32_t)npaths * (uint32_t)dim;
+    for (uint32_t k = 0; k < total;) {
+      if (pos == MT_N) {
+        mt_twist(sh->st[cur], sh->st[cur ^ 1]);
+        cur ^= 1;
+        pos = 0;
+      }
+      const uint32_t n = min((uint32_t)(MT_N - pos), total - k);
+      const uint32_t *blk = sh->st[cur] + pos;
+      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t kk = k + i;
+        const uint32_t pth = __umulhi(kk, dim_m), dd = kk - pth * (uint32_t)dim;
+        scr[dd * TILE + pth] = mt_temper(blk[i]);
+      }
+      pos += (int)n;
+      k += n;
+    }
+    __syncthreads();
+  }
+  __device__ void skip(int) {}
+  __device__ void unit(int, int npaths, int d0, int Dc, double *zt) {
+    if (d0 == 0) fill_tile(npaths);
+    for (int dd = 0; dd < Dc; dd++)
+      zt[dd * TILE + threadIdx.x] = philox_u(__ldcg(scr + (d0 + dd) * TILE + threadIdx.x));
+  }
+};
+
+// ======================================================================
 // Warp-cooperative inverse normal over the thread's own column of a chunk.
 // Comparisons run on the integer pipe (IEEE order of non-negative doubles
 // == order of their bit patterns); four inputs are in flight per pass for
@@ -1001,6 +1230,85 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
 }
 
 // ======================================================================
+// Path kernel of the sequential word streams (MT19937 / XORWOW).  Units of
+// work are (replication, segment of seg_len paths); a CTA walks its units
+// grid-stride.  Per unit the generator is positioned once (snapshot load or
+// per-thread jump) and then streams: XORWOW threads own runs of consecutive
+// paths, MT19937 tiles are TILE consecutive paths.  The model side
+// (inverse normal, path, payoff) is the same as k_paths.
+// ======================================================================
+struct ModelPoints {  // sampler.fill of a sequential stream: write the uniforms
+  static constexpr bool NORMALS = false;
+  static constexpr int MINB = 4;
+  using Shared = NoShared;
+  static __host__ __device__ int gen_dims(int dim) { return dim; }
+  __device__ void init(const ModelParams &, Shared &) {}
+  __device__ void begin() {}
+  __device__ void chunk(int, int, const double *) {}
+  __device__ double payoff() const { return 0.0; }
+};
+
+template <class G, class Mdl>
+__global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::MINB
+                                                                          : MaxBlocks<G>::value))
+    k_paths_seq(PathArgs a, SeqArgs q) {
+  extern __shared__ __align__(16) double z[];  // ZT_BYTES
+  __shared__ uint16_t tq[WARPS][CHUNK * 32];
+  __shared__ typename G::Shared gsh;
+  __shared__ typename Mdl::Shared msh;
+  constexpr bool POINTS = std::is_same<Mdl, ModelPoints>::value;
+  Mdl md;
+  md.init(a.mp, msh);
+  const int warp = threadIdx.x >> 5;
+  const int dim = a.mp.dim;
+  const int gdims = Mdl::gen_dims(dim);
+  G g;
+  g.setup(a.t, gsh, q.scratch + (size_t)blockIdx.x * dim * TILE);
+  if constexpr (!G::RUNS) g.set_seq(q, dim);
+  __syncthreads();
+  const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
+  const int64_t nunits = (int64_t)a.rep_n * q.segs_per_rep;
+#pragma unroll 1
+  for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x) {
+    const int rl = a.rep_local0 + (int)(un / q.segs_per_rep);
+    const int sg = (int)(un % q.segs_per_rep);
+    const int64_t s0 = (int64_t)sg * q.seg_len;  // path offset in [0, nmax)
+    const int slen = (int)min(q.seg_len, a.nmax - s0);
+    const int ntile = (slen + TILE - 1) / TILE;
+    const int64_t my0 = G::RUNS ? s0 + (int64_t)threadIdx.x * ntile : s0 + threadIdx.x;
+    // the whole word stream is positioned even for path-free models (gdims
+    // = 0 never reaches here for the sequential generators: no such model)
+    g.begin_segment(rl, rl - a.rep_local0, sg, q.p0 + s0, q.p0 + my0, dim);
+#pragma unroll 1
+    for (int u = 0; u < ntile; u++) {
+      const int rel = G::RUNS ? (int)threadIdx.x * ntile + u : u * TILE + (int)threadIdx.x;
+      const bool ok = rel < slen;
+      const int64_t off = s0 + rel;  // path offset of this thread in [0, nmax)
+      const int npaths = min(TILE, slen - u * TILE);
+#pragma unroll 1
+      for (int c = 0; c < nchunk; c++) {
+        const int d0 = c * CHUNK, Dc = gdims - d0 < CHUNK ? gdims - d0 : CHUNK;
+        g.unit(rl, npaths, d0, Dc, z);
+        if (d0 + Dc >= gdims) g.skip(dim - gdims);
+        __syncthreads();
+        if (d0 == 0) md.begin();
+        if constexpr (POINTS) {
+          if (ok)
+            for (int dd = 0; dd < Dc; dd++)
+              a.payoffs[off * dim + d0 + dd] = z[dd * TILE + threadIdx.x];
+        } else {
+          if (Mdl::NORMALS) chunk_to_normals(z, Dc, tq[warp]);
+          md.chunk(d0, Dc, z + threadIdx.x);
+          if (d0 + Dc >= gdims && ok)
+            a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + off] = md.payoff();
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+// ======================================================================
 // Point kernels (sampler.fill / sampler.at), out[count][dim] row-major.
 // Consecutive rows use the tiled generators, explicit indices the direct.
 // ======================================================================
@@ -1332,6 +1640,104 @@ int paths_grid_blocks(const RepTables &t, const ModelParams &mp) {
   int blocks = 0;
   paths_dispatch(a, nullptr, 0, true, &blocks);
   return blocks;
+}
+
+// ---------------------------------------------------------------- sequential streams
+cudaError_t launch_xorwow_setup(const RepTables &t, uint32_t *state, cudaStream_t s) {
+  k_xorwow_setup<<<(t.rep_count + 127) / 128, 128, 0, s>>>(t, state);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mt_snap(const RepTables &t, int rep_local0, int rep_n, const SeqArgs &q,
+                           uint32_t *snap, cudaStream_t s) {
+  k_mt_snap<<<rep_n, 256, 0, s>>>(t, rep_local0, t.dim, q, snap);
+  return cudaGetLastError();
+}
+
+template <class G, class Mdl>
+static cudaError_t seq_gm(const PathArgs &a, const SeqArgs &q, int blocks, int *launched,
+                          cudaStream_t s, int *occ) {
+  size_t dyn = prep_dyn(k_paths_seq<G, Mdl>, ZT_BYTES);
+  if (occ) {
+    *occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_paths_seq<G, Mdl>, TILE, dyn);
+    return cudaSuccess;
+  }
+  k_paths_seq<G, Mdl><<<blocks, TILE, dyn, s>>>(a, q);
+  if (launched) *launched += 1;
+  return cudaGetLastError();
+}
+
+template <class G>
+static cudaError_t seq_g(const PathArgs &a, const SeqArgs &q, int blocks, int *launched,
+                         cudaStream_t s, int *occ) {
+  switch (a.mp.kind) {
+    case MODEL_LIBOR:
+      switch (a.mp.dim) {
+        case 10: return seq_gm<G, ModelLibor<10>>(a, q, blocks, launched, s, occ);
+        case 20: return seq_gm<G, ModelLibor<20>>(a, q, blocks, launched, s, occ);
+        case 40: return seq_gm<G, ModelLibor<40>>(a, q, blocks, launched, s, occ);
+        case 80: return seq_gm<G, ModelLibor<80>>(a, q, blocks, launched, s, occ);
+      }
+      return cudaErrorInvalidValue;
+    case MODEL_MBS:
+      if (a.mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
+      return seq_gm<G, ModelMbs>(a, q, blocks, launched, s, occ);
+    case MODEL_X1: return seq_gm<G, ModelTest<false>>(a, q, blocks, launched, s, occ);
+    case MODEL_CONST1: return seq_gm<G, ModelTest<true>>(a, q, blocks, launched, s, occ);
+    case MODEL_POINTS: return seq_gm<G, ModelPoints>(a, q, blocks, launched, s, occ);
+  }
+  return cudaErrorInvalidValue;
+}
+
+static cudaError_t seq_dispatch(const PathArgs &a, const SeqArgs &q, int blocks, int *launched,
+                                cudaStream_t s, int *occ) {
+  switch (a.t.gen) {
+    case GEN_TWISTER: return seq_g<GenTwister>(a, q, blocks, launched, s, occ);
+    case GEN_XORWOW: return seq_g<GenXorwow>(a, q, blocks, launched, s, occ);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Segment length: long enough that positioning a segment (XORWOW: up to 48
+// matrix-vector products per thread, ~30k instructions; MT19937: a 2.5 KB
+// snapshot) is a few percent of its path work (~120 instructions per
+// coordinate), short enough for >= 4 units per CTA.
+void seq_layout(const RepTables &t, const ModelParams &mp, int rep_n, int64_t nmax,
+                int64_t *seg_len, int *segs_per_rep, int *blocks) {
+  PathArgs a{};
+  a.t = t;
+  a.mp = mp;
+  int occ = 1;
+  SeqArgs q{};
+  seq_dispatch(a, q, 0, nullptr, 0, &occ);
+  if (occ < 1) occ = 1;
+  const int ctas = occ * sm_count();
+  int64_t want = (int64_t)(128.0 * 1.5e6 / (120.0 * (mp.dim > 0 ? mp.dim : 1)));
+  int64_t cap = ((int64_t)rep_n * nmax) / (4 * (int64_t)ctas);
+  int64_t L = std::min(want, cap);
+  L = std::max<int64_t>(L, 8 * TILE);
+  L = (L + TILE - 1) / TILE * TILE;
+  const int64_t nm = (nmax + TILE - 1) / TILE * TILE;
+  if (L > nm) L = nm;
+  *seg_len = L;
+  *segs_per_rep = (int)((nmax + L - 1) / L);
+  const int64_t units = (int64_t)rep_n * *segs_per_rep;
+  *blocks = (int)std::min<int64_t>(units, ctas);
+}
+
+cudaError_t launch_paths_seq(const RepTables &t, const ModelParams &mp, int rep_local0,
+                             int rep_n, int64_t nmax, const SeqArgs &q, int blocks,
+                             double *payoffs, int *launched, cudaStream_t s) {
+  PathArgs a{};
+  a.t = t;
+  a.mp = mp;
+  a.rep_local0 = rep_local0;
+  a.rep_n = rep_n;
+  a.nmax = nmax;
+  a.tiles_per_rep = (nmax + TILE - 1) / TILE;
+  a.payoffs = payoffs;
+  return seq_dispatch(a, q, blocks, launched, s, nullptr);
 }
 
 cudaError_t launch_reduce(const SumPlan &plan, const double *payoffs, int64_t pay_stride,

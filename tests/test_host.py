@@ -40,9 +40,15 @@ def test_config_validation_mirrors_reference():
 
 
 def test_generators_without_device_path_raise():
-    for name in ("twister", "xorwow", "kakutani", "bogus"):
+    for name in ("kakutani", "bogus"):
         with pytest.raises(H.ConfigurationError):
             H.make_sampler(name, 2, 0, 1)
+    # the sequential word streams have a device path; they are not counter-based
+    assert {"twister", "xorwow"} <= set(H.DEVICE_GENERATORS)
+    assert not ({"twister", "xorwow"} & H.COUNTER_BASED)
+    with pytest.raises(H.ConfigurationError):
+        H.ExperimentConfig(model="libor", generator="xorwow", n_grid=(10,),
+                           paradigm="stride-parallel")
 
 
 def test_sample_std_and_slope():
