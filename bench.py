@@ -54,6 +54,22 @@ WORKLOADS = {
 NORMAL_SLOTS = 36  # Phi^-1 per normal
 
 
+# DRAM bytes (read + write) per path of the path kernel, from one
+# `ncu --set full` capture per workload (profiles/traffic.json); the
+# algorithmic traffic is the 8-byte payoff per path.
+TRAFFIC_SOURCE = "profiles/traffic.json (ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum)"
+
+
+def traffic_per_launch(workload: str, gen: str, M: int, N: int):
+    try:
+        tab = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        bpp = tab[f"{workload}/{gen}"]["dram_bytes_per_path"]
+    except (OSError, KeyError, ValueError):
+        return None
+    per_launch = min(M, max(1, (32 << 20) // N)) * N  # rq_estimate's replication batch
+    return bpp * per_launch
+
+
 def build_model(kind, maturity, accrual):
     from paper_1408_5526_b200 import models as M
 
@@ -132,7 +148,7 @@ def device_step(gen_id, model, seed, first, count, grid, theta, lib, C, _lib):
     n = C.c_int32(0)
     _lib.check(lib.rq_estimate(h, C.byref(ms), g.ctypes.data_as(C.POINTER(C.c_int64)), g.size,
                                theta.data_ptr(), C.byref(n), st))
-    return h, n.value + (1 if gen_id in (0, 1, 3, 4, 7) else 0), keep  # + setup kernel
+    return h, n.value + (1 if gen_id in (0, 1, 3, 4, 7, 8) else 0), keep  # + setup kernel
 
 
 def run_stream(args) -> dict:
@@ -322,7 +338,8 @@ def run_ours(args) -> dict:
                                                            + ks["setup_ms"], 1e-9),
                 "kernel_ms": {"setup": ks["setup_ms"], "paths": ks["paths_ms"],
                               "reduce": ks["reduce_ms"]},
-                "traffic": None,
+                "traffic": traffic_per_launch(args.workload, gen, M, N),
+                "traffic_source": TRAFFIC_SOURCE,
             },
             "e2e": {"value": e2e_value, "unit": "paths/s",
                     "h2d_bytes_per_step": tr["h2d"] // ne, "d2h_bytes_per_step": tr["d2h"] // ne,

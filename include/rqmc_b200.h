@@ -43,7 +43,8 @@ enum rq_generator {
   RQ_GEN_SOBOL_COUNTER = 4,    /* sobol.SobolCounter      sobol.py:349-372  */
   RQ_GEN_SFC64 = 5,            /* per-path SFC64 streams (numpy SFC64 core) */
   RQ_GEN_TWISTER = 6,          /* prng.MT19937 word stream  prng.py:40-82, harness.py:110-111 */
-  RQ_GEN_XORWOW = 7            /* prng.Xorwow word stream   prng.py:90-149, harness.py:112-113 */
+  RQ_GEN_XORWOW = 7,           /* prng.Xorwow word stream   prng.py:90-149, harness.py:112-113 */
+  RQ_GEN_KAKUTANI = 8          /* halton.KakutaniSampler     halton.py:521-542, harness.py:118-119 */
 };
 
 /* Model kinds: models.LiborModel (models.py:296-329), models.MbsModel
@@ -140,6 +141,10 @@ int rq_fp64_peak(double *slots_per_s, double *ms);
 /* Host-side constant tables (for tests and the Python shim). */
 int rq_sobol_directions(int dim, uint32_t *v_host); /* default_table(dim).v sobol.py:170 */
 int rq_halton_constants(int dim, int32_t *base, int32_t *K, double *scale0);
+/* Kakutani bracket tables of dims 0..dim-1 (KakutaniState._grow_tables,
+ * halton.py:178-193): thr[d][k] = float(1/p^(k+1)) + 1e-11 and
+ * b[d][k] = float((p + 1 - p^(k+1)) / p^(k+1)), 64 entries per dim. */
+int rq_kakutani_tables(int dim, double *thr_host, double *b_host);
 /* The device's division-by-base magic for dimension d, evaluated on the
  * host: q64 = floor(x / p) for x < 2^46, q32 = floor((uint32)x / p). */
 int rq_halton_divide(int d, uint64_t x, uint64_t *q64, uint32_t *q32);

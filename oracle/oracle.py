@@ -20,7 +20,8 @@ HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "build" / "librqmc_oracle.so"
 
 GEN_IDS = {"rasrap-recursive": 0, "rasrap-counter": 1, "philox": 2, "sobol-gray": 3,
-           "sobol-counter": 4, "sfc64": 5, "twister": 6, "xorwow": 7}
+           "sobol-counter": 4, "sfc64": 5, "twister": 6, "xorwow": 7,
+           "kakutani": 8}
 MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3}
 FAMILY_IDS = {"twister": 1, "xorwow": 2, "philox": 3, "rasrap": 4, "sobol": 5, "kakutani": 6,
               "sfc64": 7}
@@ -85,6 +86,9 @@ def _declare(L):
     L.orc_mt19937_words.argtypes = [C.c_void_p, i64, P(C.c_uint32)]
     L.orc_xorwow_init.argtypes = [C.c_void_p, u64]
     L.orc_xorwow_words.argtypes = [C.c_void_p, i64, P(C.c_uint32)]
+    L.orc_kakutani_set_tables.argtypes = [P(dbl), P(dbl), i32]
+    L.orc_kakutani_points.argtypes = [i32, u64, i64, P(dbl)]
+    _set_kakutani_tables(L)
 
 
 # ---------------------------------------------------------------- seeding
@@ -187,6 +191,52 @@ def sfc64_uniforms(seed: int, m: int, paths, dim: int) -> np.ndarray:
     out = np.empty((paths.size, dim))
     lib().orc_sfc64_path_uniforms(seed, m, _p(paths, C.c_int64), paths.size, dim,
                                   _p(out, C.c_double))
+    return out
+
+
+KK_TAB = 64
+_KK = {}
+
+
+def kakutani_tables(dims: int = 512):
+    """KakutaniState._grow_tables (halton.py:178-193) for the first `dims`
+    primes: thr = float(Fraction(1, p^k)) + 1e-11, b = float(Fraction(p + 1 - p^k, p^k)),
+    k = 1..64 -> arrays [dims, 64]."""
+    from fractions import Fraction
+
+    if dims not in _KK:
+        thr = np.empty((dims, KK_TAB))
+        b = np.empty((dims, KK_TAB))
+        ps = [int(p) for p in _primes_py(dims)]
+        for d, p in enumerate(ps):
+            pk = 1
+            for k in range(1, KK_TAB + 1):
+                pk *= p
+                b[d, k - 1] = float(Fraction(p + 1 - pk, pk))
+                thr[d, k - 1] = float(Fraction(1, pk)) + 1e-11
+        _KK[dims] = (thr, b)
+    return _KK[dims]
+
+
+def _primes_py(n: int):
+    out, c = [], 2
+    while len(out) < n:
+        if all(c % q for q in out if q * q <= c):
+            out.append(c)
+        c += 1
+    return out
+
+
+def _set_kakutani_tables(L):
+    thr, b = kakutani_tables(512)
+    L.orc_kakutani_set_tables(_p(thr, C.c_double), _p(b, C.c_double), thr.shape[0])
+
+
+def kakutani_points(dim: int, key: int, count: int) -> np.ndarray:
+    """KakutaniSampler(dim, key).fill of `count` rows (halton.py:521-542)."""
+    out = np.empty((count, dim))
+    if lib().orc_kakutani_points(dim, key & 0xFFFFFFFFFFFFFFFF, count, _p(out, C.c_double)):
+        raise ValueError("kakutani orbit left the 64-entry bracket tables")
     return out
 
 

@@ -727,18 +727,102 @@ void orc_xorwow_words(orc_xorwow *g, int64_t n, uint32_t *out) {
 }
 
 /* ------------------------------------------------------------------ */
+/* Kakutani orbits (halton.py:163-239, 521-542)                          */
+/* ------------------------------------------------------------------ */
+
+/* Bracket tables per dimension, [dims][64] (KakutaniState._grow_tables,
+ * halton.py:178-193): exact rationals rounded by Python; set by oracle.py. */
+static const double *KK_THR = NULL, *KK_B = NULL;
+static int KK_DIMS = 0;
+#define KK_TAB 64
+
+void orc_kakutani_set_tables(const double *thr, const double *b, int dims) {
+  KK_THR = thr;
+  KK_B = b;
+  KK_DIMS = dims;
+}
+
+/* kakutani_next (halton.py:208-239): log guess, then the two bracket loops */
+static int kak_next(double *x, int d, int64_t p) {
+  const double *thr = KK_THR + (size_t)d * KK_TAB, *b = KK_B + (size_t)d * KK_TAB;
+  double one_minus = 1.0 - *x;
+  int k = (int)(-log(one_minus) / log((double)p)) + 1;
+  if (k < 1) k = 1;
+  if (k + 1 > KK_TAB) return -1;
+  while (one_minus <= thr[k - 1]) {
+    k++;
+    if (k + 1 > KK_TAB) return -1;
+  }
+  while (k > 1 && one_minus > thr[k - 2]) k--;
+  double v = *x + b[k - 1];
+  if (v >= 1.0) v -= 1.0;
+  *x = v;
+  return 0;
+}
+
+typedef struct {
+  int dim, emitted;
+  double *x;
+  int64_t *base;
+} kak_sampler;
+
+static int kak_init(kak_sampler *s, int dim, uint64_t key) {
+  if (!KK_THR || dim > KK_DIMS) return -1;
+  s->dim = dim;
+  s->emitted = 0;
+  s->x = (double *)malloc(sizeof(double) * dim);
+  s->base = (int64_t *)malloc(sizeof(int64_t) * dim);
+  orc_primes(dim, s->base);
+  for (int d = 0; d < dim; d++) { /* derive_rng(seed, i).random() (halton.py:532-534) */
+    uint64_t parts[2] = {key, (uint64_t)d};
+    orc_pcg64 g;
+    orc_pcg64_seed(&g, orc_derive_key(parts, 2));
+    s->x[d] = orc_pcg64_random(&g);
+  }
+  return 0;
+}
+
+/* KakutaniSampler.fill (halton.py:536-542) */
+static int kak_fill(kak_sampler *s, int64_t n, double *out) {
+  for (int64_t i = 0; i < n; i++) {
+    if (!s->emitted) {
+      s->emitted = 1;
+    } else {
+      for (int d = 0; d < s->dim; d++)
+        if (kak_next(&s->x[d], d, s->base[d])) return -1;
+    }
+    for (int d = 0; d < s->dim; d++) out[i * s->dim + d] = s->x[d];
+  }
+  return 0;
+}
+
+static void kak_free(kak_sampler *s) {
+  free(s->x);
+  free(s->base);
+}
+
+int orc_kakutani_points(int dim, uint64_t key, int64_t count, double *out) {
+  kak_sampler s;
+  if (kak_init(&s, dim, key)) return -1;
+  int rc = kak_fill(&s, count, out);
+  kak_free(&s);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ */
 /* harness.py replication loop                                          */
 /* ------------------------------------------------------------------ */
 
 #define CHUNK_PATHS 8192 /* harness.py:25 */
 
-/* seeding.py:17-24 (twister 1, xorwow 2, philox 3, rasrap 4, sobol 5); 7 = sfc64 */
-static const uint64_t FAMILY_ID[8] = {4, 4, 3, 5, 5, 7, 1, 2};
+/* seeding.py:17-24 (twister 1, xorwow 2, philox 3, rasrap 4, sobol 5, kakutani 6);
+ * 7 = sfc64 */
+static const uint64_t FAMILY_ID[9] = {4, 4, 3, 5, 5, 7, 1, 2, 6};
 
 int orc_run_replication(int gen, int model, int dim, const double *mparams, uint64_t seed,
                         int64_t m, const int64_t *grid, int ngrid, const uint32_t *sobol_v,
                         double *theta) {
-  if (gen < 0 || gen > 7 || model < 0 || model > 3 || ngrid < 1) return -1;
+  if (gen < 0 || gen > 8 || model < 0 || model > 3 || ngrid < 1) return -1;
   int64_t nmax = grid[ngrid - 1];
   uint64_t parts[3] = {seed, FAMILY_ID[gen], (uint64_t)m};
   uint64_t key = orc_derive_key(parts, 3); /* harness.py:113 */
@@ -751,6 +835,8 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
   rasrap_cfg cfg;
   orc_mt19937 mt;
   orc_xorwow xw;
+  kak_sampler kk;
+  if (gen == 8 && kak_init(&kk, dim, key)) return -1;
   if (gen == 6) orc_mt19937_init(&mt, (uint32_t)key); /* harness.py:111 key & 0xFFFFFFFF */
   if (gen == 7) orc_xorwow_init(&xw, key);             /* harness.py:113 */
   if (gen == 0) rec_init(&rec, dim, key);
@@ -760,11 +846,17 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
     shift = (uint32_t *)malloc(sizeof(uint32_t) * dim);
     orc_sobol_scramble(dim, sobol_v, key, m, gen_v, shift); /* harness.py:122 */
   }
+  int rc = 0;
   for (int64_t done = 0; done < nmax;) {
     int64_t cnt = nmax - done < CHUNK_PATHS ? nmax - done : CHUNK_PATHS;
     for (int64_t i = 0; i < cnt; i++) idx[i] = done + i;
     if (gen == 0) {
       rec_fill(&rec, cnt, buf);
+    } else if (gen == 8) {
+      if (kak_fill(&kk, cnt, buf)) {
+        rc = -1;
+        break;
+      }
     } else if (gen == 1) {
       counter_points(&cfg, idx, cnt, buf);
     } else if (gen == 5) {
@@ -798,8 +890,9 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
     }
     done += cnt;
   }
-  for (int g = 0; g < ngrid; g++)
+  for (int g = 0; rc == 0 && g < ngrid; g++)
     theta[g] = orc_pairwise_sum(payoffs, grid[g]) / (double)grid[g]; /* harness.py:314 */
+  if (gen == 8) kak_free(&kk);
   if (gen == 0) rec_free(&rec);
   if (gen == 1) cfg_free(&cfg);
   free(gen_v);
@@ -808,7 +901,7 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
   free(idx);
   free(buf);
   free(payoffs);
-  return 0;
+  return rc;
 }
 
 typedef struct {

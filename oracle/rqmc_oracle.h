@@ -88,7 +88,7 @@ double orc_pairwise_sum(const double *a, int64_t n);
  * estimates theta[g] = np.sum(payoffs[:grid[g]]) / grid[g].
  * gen: 0 rasrap-recursive, 1 rasrap-counter, 2 philox, 3 sobol-gray,
  *      4 sobol-counter, 5 sfc64 (builder-defined per-path streams), 6 twister,
- *      7 xorwow.  model: 0 libor, 1 mbs, 2 x1, 3 const1.
+ *      7 xorwow, 8 kakutani (needs orc_kakutani_set_tables).  model: 0 libor, 1 mbs, 2 x1, 3 const1.
  * mparams: libor {delta, sigma, strike, front_factor, l0[steps]...};
  *          mbs {i0,k0,k1,k2,k3,k4,sigma_xi,payment, ck[months]...}.
  * sobol_v: unscrambled direction words [dim x 32] (gen 3/4 only). */
@@ -113,6 +113,12 @@ typedef struct {
 } orc_xorwow;
 void orc_xorwow_init(orc_xorwow *g, uint64_t seed);
 void orc_xorwow_words(orc_xorwow *g, int64_t n, uint32_t *out);
+
+/* Kakutani orbits (halton.py:163-239, 521-542).  The bracket tables
+ * [dims][64] (thr = float(1/p^k) + 1e-11, b = float((p+1-p^k)/p^k)) come
+ * from oracle.py, computed with fractions.Fraction as the reference does. */
+void orc_kakutani_set_tables(const double *thr, const double *b, int dims);
+int orc_kakutani_points(int dim, uint64_t key, int64_t count, double *out);
 
 /* SFC64 (no reference counterpart; numpy.random.SFC64 is the oracle).
  * Per-path stream seeded from derive_words(derive_key(seed, 7, m, path), 6). */

@@ -29,6 +29,7 @@ GEN_IDS = {
     "sfc64": 5,
     "twister": 6,
     "xorwow": 7,
+    "kakutani": 8,
 }
 MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3}
 
@@ -90,11 +91,13 @@ def _declare(L):
     L.rq_sobol_directions.argtypes = [C.c_int, P(C.c_uint32)]
     L.rq_halton_constants.argtypes = [C.c_int, P(C.c_int32), P(C.c_int32), P(dbl)]
     L.rq_halton_divide.argtypes = [C.c_int, u64, P(u64), P(C.c_uint32)]
+    L.rq_kakutani_tables.argtypes = [C.c_int, P(dbl), P(dbl)]
     for name in ("rq_sampler_create", "rq_sampler_points", "rq_sampler_points_at",
                  "rq_sampler_rasrap_tables", "rq_estimate", "rq_run_replications",
                  "rq_model_payoffs", "rq_inv_normal", "rq_stream_normals", "rq_pairwise_sum",
                  "rq_pairwise_sum_host", "rq_fp64_peak",
-                 "rq_sobol_directions", "rq_halton_constants", "rq_halton_divide"):
+                 "rq_sobol_directions", "rq_halton_constants", "rq_halton_divide",
+                 "rq_kakutani_tables"):
         getattr(L, name).restype = C.c_int
 
 

@@ -184,6 +184,124 @@ std::vector<uint32_t> xorwow_jump_columns() {
   return cols;
 }
 
+// ---- Kakutani bracket tables (halton.py:178-193): the correctly rounded
+// doubles of the exact rationals 1/p^k and (p + 1 - p^k)/p^k, k = 1..64, as
+// the reference computes them with fractions.Fraction; thr = inv + 1e-11
+// in double arithmetic (halton.py:231).
+using Big = std::vector<uint32_t>;  // little-endian 32-bit limbs
+void big_mul_small(Big &a, uint32_t m) {
+  uint64_t c = 0;
+  for (auto &w : a) {
+    uint64_t t = (uint64_t)w * m + c;
+    w = (uint32_t)t;
+    c = t >> 32;
+  }
+  if (c) a.push_back((uint32_t)c);
+}
+int big_bits(const Big &a) {
+  for (int i = (int)a.size() - 1; i >= 0; i--)
+    if (a[i]) return i * 32 + 32 - __builtin_clz(a[i]);
+  return 0;
+}
+int big_cmp(const Big &a, const Big &b) {
+  size_t n = std::max(a.size(), b.size());
+  for (int i = (int)n - 1; i >= 0; i--) {
+    uint32_t x = i < (int)a.size() ? a[i] : 0u, y = i < (int)b.size() ? b[i] : 0u;
+    if (x != y) return x < y ? -1 : 1;
+  }
+  return 0;
+}
+void big_sub(Big &a, const Big &b) {  // a -= b, a >= b
+  int64_t br = 0;
+  for (size_t i = 0; i < a.size(); i++) {
+    int64_t t = (int64_t)a[i] - (i < b.size() ? b[i] : 0u) - br;
+    br = t < 0;
+    a[i] = (uint32_t)(t + (br ? ((int64_t)1 << 32) : 0));
+  }
+}
+Big big_shl(const Big &a, int bits) {
+  Big r((size_t)(bits / 32), 0u);
+  uint32_t c = 0;
+  const int sh = bits % 32;
+  for (uint32_t w : a) {
+    r.push_back(sh ? (w << sh) | c : w);
+    c = sh ? w >> (32 - sh) : 0u;
+  }
+  if (c) r.push_back(c);
+  return r;
+}
+// n / d rounded to nearest (ties to even), 0 < n < d
+double big_ratio(const Big &n, const Big &d) {
+  const int ln = big_bits(n), ld = big_bits(d);
+  const int s = 54 + ld - ln;  // n 2^s / d in [2^53, 2^55), s >= 54
+  Big r = big_shl(n, s - 55 > 0 ? s - 55 : 0);
+  const int iters = s < 55 ? s : 55;
+  uint64_t q = 0;
+  for (int i = 0; i < iters; i++) {
+    r = big_shl(r, 1);
+    q <<= 1;
+    if (big_cmp(r, d) >= 0) {
+      big_sub(r, d);
+      q |= 1;
+    }
+  }
+  bool sticky = big_bits(r) != 0;
+  int e = -s;
+  if (q >> 54) {
+    sticky |= q & 1;
+    q >>= 1;
+    e++;
+  }
+  uint64_t m = q >> 1;
+  if ((q & 1) && (sticky || (m & 1))) m++;
+  return std::ldexp((double)m, e + 1);
+}
+void kakutani_tables(int p, double *thr, double *b) {
+  Big pk{1u};
+  for (int k = 1; k <= rq::KK_TAB; k++) {
+    big_mul_small(pk, (uint32_t)p);
+    const double inv = big_ratio(Big{1u}, pk);
+    thr[k - 1] = inv + 1e-11;  // halton.py:205 _BRACKET_TOL
+    if (k == 1) {
+      b[0] = inv;  // (p + 1 - p) / p
+    } else {
+      Big num = pk;  // p^k - p - 1
+      big_sub(num, Big{(uint32_t)p + 1u});
+      b[k - 1] = -big_ratio(num, pk);
+    }
+  }
+}
+const std::vector<double> &kakutani_host_tables() {  // [MAX_DIM][2][KK_TAB]
+  static std::vector<double> T;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const HostTables &H = host_tables();
+    T.resize((size_t)rq::MAX_DIM * 2 * rq::KK_TAB);
+    for (int d = 0; d < rq::MAX_DIM; d++)
+      kakutani_tables(H.dims[d].base, &T[(size_t)d * 2 * rq::KK_TAB],
+                      &T[(size_t)d * 2 * rq::KK_TAB + rq::KK_TAB]);
+  });
+  return T;
+}
+int ensure_kakutani_tables() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  RQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return RQ_OK;
+  const std::vector<double> &T = kakutani_host_tables();
+  std::vector<double> thr((size_t)rq::MAX_DIM * rq::KK_TAB), b(thr.size());
+  for (int d = 0; d < rq::MAX_DIM; d++)
+    for (int k = 0; k < rq::KK_TAB; k++) {
+      thr[(size_t)d * rq::KK_TAB + k] = T[(size_t)d * 2 * rq::KK_TAB + k];
+      b[(size_t)d * rq::KK_TAB + k] = T[(size_t)d * 2 * rq::KK_TAB + rq::KK_TAB + k];
+    }
+  RQ_CUDA(rq::upload_kakutani_tables(thr.data(), b.data(), rq::MAX_DIM));
+  done.push_back(dev);
+  return RQ_OK;
+}
+
 int ensure_device_tables() {
   static std::mutex mu;
   static std::vector<int> done;
@@ -366,6 +484,17 @@ int rq_halton_divide(int d, uint64_t x, uint64_t *q64, uint32_t *q32) {
   return RQ_OK;
 }
 
+int rq_kakutani_tables(int dim, double *thr_host, double *b_host) {
+  if (dim < 1 || dim > rq::MAX_DIM) return fail(RQ_ERR_VALUE, "dim %d outside 1..%d", dim, rq::MAX_DIM);
+  const std::vector<double> &T = kakutani_host_tables();
+  for (int d = 0; d < dim; d++)
+    for (int k = 0; k < rq::KK_TAB; k++) {
+      if (thr_host) thr_host[(size_t)d * rq::KK_TAB + k] = T[(size_t)d * 2 * rq::KK_TAB + k];
+      if (b_host) b_host[(size_t)d * rq::KK_TAB + k] = T[(size_t)d * 2 * rq::KK_TAB + rq::KK_TAB + k];
+    }
+  return RQ_OK;
+}
+
 int rq_halton_constants(int dim, int32_t *base, int32_t *K, double *scale0) {
   if (dim < 1 || dim > rq::MAX_DIM) return fail(RQ_ERR_VALUE, "dim %d outside 1..%d", dim, rq::MAX_DIM);
   const HostTables &T = host_tables();
@@ -470,6 +599,26 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
     }
     t.sobol_v = gen;
     t.sobol_shift = sh;
+  } else if (generator == rq::GEN_KAKUTANI) {
+    if (dim > rq::MAX_DIM) {
+      delete S;
+      return fail(RQ_ERR_VALUE, "kakutani dimension %d exceeds %d", dim, rq::MAX_DIM);
+    }
+    if ((rc = ensure_kakutani_tables())) {
+      delete S;
+      return rc;
+    }
+    cudaError_t e = cudaMallocAsync(&S->mem, sizeof(double) * dim * rep_count, s);
+    if (e == cudaSuccess) {
+      KTimer kt(&g_stats.setup_ms, s);
+      e = rq::launch_kakutani_setup(t, (double *)S->mem, s);
+    }
+    if (e != cudaSuccess) {
+      if (S->mem) cudaFreeAsync(S->mem, s);
+      delete S;
+      return fail(RQ_ERR_CUDA, "kakutani setup: %s", cudaGetErrorString(e));
+    }
+    t.kk_x0 = (const double *)S->mem;
   } else if (generator == rq::GEN_XORWOW) {
     cudaError_t e = cudaMallocAsync(&S->mem, sizeof(uint32_t) * 6 * rep_count, s);
     if (e == cudaSuccess) {
@@ -496,6 +645,7 @@ struct SeqRun {
   int ctas = 0;
   int64_t grp0 = 0, grpn = 0, grp_cap = 0;
   uint32_t *snap = nullptr;
+  size_t per_rep = 0;  // snapshot bytes per replication
   void *mem = nullptr;
   cudaStream_t stream = nullptr;  // the work stream: freed in stream order
   ~SeqRun() {
@@ -510,16 +660,19 @@ static int seq_begin(const rq::RepTables &t, const rq::ModelParams &mp, int B, i
   R.q.p0 = p0;
   R.q.seg_len = L;
   R.q.segs_per_rep = segs;
-  if (t.gen != rq::GEN_TWISTER) return RQ_OK;
-  const size_t per_rep = sizeof(uint32_t) * rq::MT_N * (size_t)segs;
+  if (t.gen == rq::GEN_XORWOW) return RQ_OK;
+  const bool mt = t.gen == rq::GEN_TWISTER;
+  const size_t per_rep = mt ? sizeof(uint32_t) * rq::MT_N * (size_t)segs
+                            : sizeof(double) * t.dim * (size_t)segs;
   int64_t G = std::max<int64_t>(B, ((int64_t)256 << 20) / (int64_t)per_rep / B * B);
   G = std::min<int64_t>(G, t.rep_count);
   R.grp_cap = G;
-  size_t b_scr = sizeof(uint32_t) * (size_t)R.ctas * t.dim * 128;
+  size_t b_scr = (mt ? sizeof(uint32_t) : sizeof(double)) * (size_t)R.ctas * t.dim * 128;
   RQ_CUDA(cudaMallocAsync(&R.mem, per_rep * G + b_scr, s));
   R.stream = s;
   R.snap = (uint32_t *)R.mem;
-  R.q.scratch = R.snap + (size_t)rq::MT_N * segs * G;
+  R.per_rep = per_rep;
+  R.q.scratch = (uint32_t *)((char *)R.mem + per_rep * G);
   R.grpn = 0;
   return RQ_OK;
 }
@@ -527,15 +680,19 @@ static int seq_begin(const rq::RepTables &t, const rq::ModelParams &mp, int B, i
 static int seq_batch(const rq::RepTables &t, int r0, int rn, SeqRun &R, int *blocks,
                      int *launched, cudaStream_t s) {
   *blocks = (int)std::min<int64_t>((int64_t)rn * R.q.segs_per_rep, R.ctas);
-  if (t.gen != rq::GEN_TWISTER) return RQ_OK;
+  if (t.gen == rq::GEN_XORWOW) return RQ_OK;
+  const bool mt = t.gen == rq::GEN_TWISTER;
   if (r0 < R.grp0 || r0 + rn > R.grp0 + R.grpn) {
     R.grp0 = r0;
     R.grpn = std::min<int64_t>(R.grp_cap, t.rep_count - r0);
     KTimer kt(&g_stats.setup_ms, s);
-    RQ_CUDA(rq::launch_mt_snap(t, r0, (int)R.grpn, R.q, R.snap, s));
+    if (mt) RQ_CUDA(rq::launch_mt_snap(t, r0, (int)R.grpn, R.q, R.snap, s));
+    else RQ_CUDA(rq::launch_kak_snap(t, r0, (int)R.grpn, R.q, (double *)R.snap, s));
     if (launched) *launched += 1;
   }
-  R.q.mt_snap = R.snap + (size_t)rq::MT_N * R.q.segs_per_rep * (r0 - R.grp0);
+  const char *at = (const char *)R.snap + R.per_rep * (size_t)(r0 - R.grp0);
+  if (mt) R.q.mt_snap = (const uint32_t *)at;
+  else R.q.kk_snap = (const double *)at;
   return RQ_OK;
 }
 
@@ -739,7 +896,7 @@ int rq_run_replications(int generator, const rq_model *model, uint64_t seed, int
     if ((rc = rq_sampler_create(&S, generator, model ? model->dim : 0, seed, rep_first + r0, rn, st)))
       return rc;
     if (kernel_launches && generator != rq::GEN_PHILOX && generator != rq::GEN_SFC64 &&
-        generator != rq::GEN_TWISTER)
+        generator != rq::GEN_TWISTER)  // (kakutani / xorwow: their start kernels)
       *kernel_launches += 1;  // the randomisation setup kernel
     rc = rq_estimate(S, model, grid_host, ngrid, theta_dev + r0 * ngrid, kernel_launches, st);
     RQ_CUDA(cudaStreamSynchronize(st));

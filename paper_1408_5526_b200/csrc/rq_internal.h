@@ -21,11 +21,13 @@ enum Gen : int {
   GEN_SFC64 = 5,
   GEN_TWISTER = 6,  // MT19937 word stream (prng.py:40-82), one per replication
   GEN_XORWOW = 7,   // XORWOW word stream (prng.py:90-149), one per replication
+  GEN_KAKUTANI = 8, // Kakutani orbits (halton.py:163-239, 521-542), one per (replication, dim)
 };
-constexpr int GEN_LAST = GEN_XORWOW;
+constexpr int GEN_LAST = GEN_KAKUTANI;
 __host__ __device__ constexpr bool gen_sequential(int g) {
-  return g == GEN_TWISTER || g == GEN_XORWOW;
+  return g == GEN_TWISTER || g == GEN_XORWOW || g == GEN_KAKUTANI;
 }
+constexpr int KK_TAB = 64;  // Kakutani bracket table entries per base (halton.py:182, 64)
 constexpr int MT_N = 624;       // MT19937 state words
 constexpr int XW_JUMPS = 48;    // XORWOW jump matrices A^(2^k), k < XW_JUMPS
 constexpr int XW_COLW = 8;      // words per matrix column (5 used, padded for 128-bit loads)
@@ -74,6 +76,8 @@ struct RepTables {
   const uint32_t *sobol_shift; // [rep][dim]
   // XORWOW: per-replication initial state (x, y, z, w, v, d) (prng.py:128-134)
   const uint32_t *xw_state;    // [rep][6]
+  // Kakutani: random starts x0 (halton.py:532-534)
+  const double *kk_x0;         // [rep][dim]
 };
 
 // Segments of the sequential word streams (MT19937 / XORWOW).  A
@@ -88,7 +92,8 @@ struct SeqArgs {
   int32_t segs_per_rep;
   const uint32_t *mt_snap;  // [rep - rep_local0][seg][MT_N] raw MT state after the twist that
                             // produced the segment's first word
-  uint32_t *scratch;        // [gridDim][dim][TILE] tempered MT words of a tile
+  const double *kk_snap;    // [rep - rep_local0][seg][dim] Kakutani orbit points at segment starts
+  uint32_t *scratch;        // [gridDim][dim][TILE] tempered MT words (Kakutani: doubles) of a tile
 };
 
 struct ModelParams {
@@ -127,6 +132,10 @@ cudaError_t launch_paths(const RepTables &t, const ModelParams &mp, int rep_loca
                          int rep_n, int64_t nmax, double *payoffs, int *launched,
                          cudaStream_t s);
 cudaError_t upload_xorwow_jumps(const uint32_t *cols, size_t words);
+cudaError_t upload_kakutani_tables(const double *thr, const double *b, int dims);
+cudaError_t launch_kakutani_setup(const RepTables &t, double *x0, cudaStream_t s);
+cudaError_t launch_kak_snap(const RepTables &t, int rep_local0, int rep_n, const SeqArgs &q,
+                            double *snap, cudaStream_t s);
 cudaError_t launch_xorwow_setup(const RepTables &t, uint32_t *state, cudaStream_t s);
 // choose the segment length / grid of the sequential-stream path kernel
 void seq_layout(const RepTables &t, const ModelParams &mp, int rep_n, int64_t nmax,

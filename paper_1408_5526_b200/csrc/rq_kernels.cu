@@ -855,6 +855,135 @@ struct GenTwister {
 };
 
 // ======================================================================
+// Kakutani orbits (halton.py:163-239, 521-542): per dimension the random
+// start x0 = derive_rng(key, d).random() and x <- x + b_k with k the
+// bracket of 1 - x.  The reference guesses k from a logarithm and then
+// corrects it until inv_pow[k-1] + tol < 1 - x <= inv_pow[k-2] + tol holds
+// (halton.py:226-235); that k is unique (the smallest k with
+// 1 - x > thr[k-1], thr = inv_pow + tol in double), so the device scans the
+// thresholds directly.  Orbits are sequential: segments start from
+// snapshots taken by k_kak_snap.
+// ======================================================================
+__device__ double g_kk_thr[MAX_DIM * KK_TAB];
+__device__ double g_kk_b[MAX_DIM * KK_TAB];
+
+cudaError_t upload_kakutani_tables(const double *thr, const double *b, int dims) {
+  cudaError_t e = cudaMemcpyToSymbol(g_kk_thr, thr, sizeof(double) * dims * KK_TAB);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(g_kk_b, b, sizeof(double) * dims * KK_TAB);
+}
+
+// One orbit step, the first two brackets (probability 1 - 1/p^2) in
+// registers, off the L1 latency chain of the sequential orbit.
+struct KakDim {
+  const double *thr, *b;
+  double t0, t1, b0, b1;
+  __device__ void load(int d) {
+    thr = g_kk_thr + d * KK_TAB;
+    b = g_kk_b + d * KK_TAB;
+    t0 = thr[0];
+    t1 = thr[1];
+    b0 = b[0];
+    b1 = b[1];
+  }
+  __device__ __forceinline__ double step(double x) const {
+    const double om = 1.0 - x;
+    double v;
+    if (om > t0) {
+      v = x + b0;
+    } else if (om > t1) {
+      v = x + b1;
+    } else {
+      int k = 2;
+      while (k < KK_TAB - 1 && om <= thr[k]) k++;
+      v = x + b[k];
+    }
+    return v >= 1.0 ? v - 1.0 : v;
+  }
+};
+
+// x0 of every (replication, dim): KakutaniState(p, rng.random()) with
+// rng = derive_rng(derive_key(seed, 6, m), d) (halton.py:530-534).
+__global__ void k_kakutani_setup(RepTables t, double *x0) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)t.rep_count * t.dim) return;
+  const int rl = (int)(gid / t.dim), d = (int)(gid % t.dim);
+  const uint64_t key = derive_key3(t.seed, 6, (uint64_t)(t.rep_first + rl));
+  Pcg64 g;
+  pcg_seed(g, derive_key2(key, (uint64_t)d));
+  x0[gid] = pcg_random(g);
+}
+
+// Orbit points at the segment starts P_s = p0 + s seg_len, one thread per
+// (replication of the group, dim); point n is x after n steps.
+__global__ void k_kak_snap(RepTables t, int rep_local0, int rep_n, SeqArgs q, double *snap) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)rep_n * t.dim) return;
+  const int rb = (int)(gid / t.dim), d = (int)(gid % t.dim);
+  KakDim kd;
+  kd.load(d);
+  double x = t.kk_x0[(int64_t)(rep_local0 + rb) * t.dim + d];
+  int64_t pos = 0;
+  for (int sg = 0; sg < q.segs_per_rep; sg++) {
+    const int64_t P = q.p0 + (int64_t)sg * q.seg_len;
+#pragma unroll 4
+    for (; pos < P; pos++) x = kd.step(x);
+    snap[((int64_t)rb * q.segs_per_rep + sg) * t.dim + d] = x;
+  }
+}
+
+// Tile layout (TILE consecutive paths): at chunk 0 of a tile, thread t
+// advances the orbits of dims t, t + TILE, ... over the tile's paths into
+// the per-CTA scratch [dim][TILE] (doubles); chunks read their columns.
+struct GenKakutani {
+  static constexpr bool RUNS = false;
+  struct Shared {
+    double xs[MAX_DIM];  // orbit state of every dim between tiles
+  };
+  const RepTables *t;
+  Shared *sh;
+  double *scr;
+  const SeqArgs *q;
+  int dim;
+  __device__ void setup(const RepTables &t_, Shared &s, uint32_t *) {
+    t = &t_;
+    sh = &s;
+  }
+  __device__ void set_seq(const SeqArgs &q_, int dim_) {
+    q = &q_;
+    dim = dim_;
+    // this CTA's slice of the scratch, [dim][TILE] doubles
+    scr = reinterpret_cast<double *>(q_.scratch) + (size_t)blockIdx.x * dim_ * TILE;
+  }
+  __device__ void begin_segment(int, int rb, int sg, int64_t, int64_t, int) {
+    const double *src = q->kk_snap + ((int64_t)rb * q->segs_per_rep + sg) * dim;
+    __syncthreads();  // the previous segment's last tile is done with xs
+    for (int d = threadIdx.x; d < dim; d += TILE) sh->xs[d] = src[d];
+  }
+  __device__ void skip(int) {}
+  __device__ void fill_tile(int npaths) {
+#pragma unroll 1
+    for (int d = threadIdx.x; d < dim; d += TILE) {
+      KakDim kd;
+      kd.load(d);
+      double xv = sh->xs[d];
+#pragma unroll 4
+      for (int j = 0; j < npaths; j++) {
+        scr[d * TILE + j] = xv;
+        xv = kd.step(xv);
+      }
+      sh->xs[d] = xv;
+    }
+    __syncthreads();
+  }
+  __device__ void unit(int, int npaths, int d0, int Dc, double *zt) {
+    if (d0 == 0) fill_tile(npaths);
+    for (int dd = 0; dd < Dc; dd++)
+      zt[dd * TILE + threadIdx.x] = __ldcg(scr + (d0 + dd) * TILE + threadIdx.x);
+  }
+};
+
+// ======================================================================
 // Warp-cooperative inverse normal over the thread's own column of a chunk.
 // Comparisons run on the integer pipe (IEEE order of non-negative doubles
 // == order of their bit patterns); four inputs are in flight per pass for
@@ -1648,6 +1777,19 @@ cudaError_t launch_xorwow_setup(const RepTables &t, uint32_t *state, cudaStream_
   return cudaGetLastError();
 }
 
+cudaError_t launch_kakutani_setup(const RepTables &t, double *x0, cudaStream_t s) {
+  const int64_t n = (int64_t)t.rep_count * t.dim;
+  k_kakutani_setup<<<(int)((n + 127) / 128), 128, 0, s>>>(t, x0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kak_snap(const RepTables &t, int rep_local0, int rep_n, const SeqArgs &q,
+                            double *snap, cudaStream_t s) {
+  const int64_t n = (int64_t)rep_n * t.dim;
+  k_kak_snap<<<(int)((n + 127) / 128), 128, 0, s>>>(t, rep_local0, rep_n, q, snap);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mt_snap(const RepTables &t, int rep_local0, int rep_n, const SeqArgs &q,
                            uint32_t *snap, cudaStream_t s) {
   k_mt_snap<<<rep_n, 256, 0, s>>>(t, rep_local0, t.dim, q, snap);
@@ -1695,6 +1837,7 @@ static cudaError_t seq_dispatch(const PathArgs &a, const SeqArgs &q, int blocks,
   switch (a.t.gen) {
     case GEN_TWISTER: return seq_g<GenTwister>(a, q, blocks, launched, s, occ);
     case GEN_XORWOW: return seq_g<GenXorwow>(a, q, blocks, launched, s, occ);
+    case GEN_KAKUTANI: return seq_g<GenKakutani>(a, q, blocks, launched, s, occ);
   }
   return cudaErrorInvalidValue;
 }

@@ -80,6 +80,7 @@ def main():
             globals()[f"_section_{sec}"](out, versions, H, M, prng, seeding)
         return
     _section_seq(out, versions, H, M, prng, seeding)
+    _section_kak(out, versions, H, M, prng, seeding)
 
     # ---------------- seeding + randomisation ---------------------------
     fams = sorted(seeding.GENERATOR_IDS.values())
@@ -256,6 +257,32 @@ def _section_seq(out, versions, H, M, prng, seeding):
         tz[f"{tag}_std"] = np.array([rep.row(gen, n).std for n in grid])
         print(tag, tz[f"{tag}_mean"], flush=True)
     np.savez_compressed(out / "theta_seq.npz", **tz)
+
+
+def _section_kak(out, versions, H, M, prng, seeding):
+    """Kakutani orbits (halton.py:163-239, 521-542): points and estimates."""
+    import time
+
+    z = {"versions": versions}
+    for dim, m, nmax in ((20, 1, 60_000), (5, 2, 200_000), (360, 1, 2000)):
+        tag = f"d{dim}_m{m}"
+        rows = _rows(nmax, head=300, step=997)
+        z[f"{tag}_rows"] = rows
+        t0 = time.time()
+        z[f"{tag}_points"] = _fill_rows(H.make_sampler("kakutani", dim, SEED, m), dim, nmax, rows)
+        print(tag, f"{time.time() - t0:.1f}s", flush=True)
+    s20 = M.LiborModel(M.LiborConfig(maturity=5.0, accrual=0.25))
+    for tag, mname, grid, reps, model in (
+            ("libor20", "libor", (1000, 8192), 4, s20),
+            ("mbs", "mbs", (500,), 2, M.MbsModel()),
+            ("x1", "x1", (7, 1000, 20_000), 4, M.FirstCoordinateModel())):
+        cfg = H.ExperimentConfig(model=mname, generator="kakutani", n_grid=grid,
+                                 replications=reps, seed=SEED, workers=4)
+        rep = H.run_experiment(cfg, model=model)
+        z[f"{tag}_grid"] = np.array(grid, dtype=np.int64)
+        z[f"{tag}_theta"] = np.stack([rep.estimates("kakutani", n) for n in grid])
+        print(tag, z[f"{tag}_theta"][:, 0], flush=True)
+    np.savez_compressed(out / "kakutani.npz", **z)
 
 
 def _words(gen, n: int) -> np.ndarray:

@@ -138,3 +138,17 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(_lib.DeviceError):
         P.run_experiment(P.ExperimentConfig(model="x1", generator="philox", n_grid=(8,),
                                             replications=2))
+
+
+def test_kakutani_tables_exact(lib, oracle):
+    """The library's big-integer rounding == the reference's Fraction tables."""
+    import ctypes as C
+
+    dims = 512
+    thr = np.empty((dims, 64))
+    b = np.empty((dims, 64))
+    assert lib.rq_kakutani_tables(dims, thr.ctypes.data_as(C.POINTER(C.c_double)),
+                                  b.ctypes.data_as(C.POINTER(C.c_double))) == 0
+    rthr, rb = oracle.kakutani_tables(dims)
+    assert np.array_equal(thr, rthr)
+    assert np.array_equal(b, rb)

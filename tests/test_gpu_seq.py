@@ -162,3 +162,60 @@ def test_theta_invariant_to_sharding(P):
         a = estimate_replications(gen, model, SEED, 1, 2, (4096,))
         b = estimate_replications(gen, model, SEED, 3, 4, (4096,))
         assert np.array_equal(full, np.concatenate([a, b]))
+
+
+# ---------------------------------------------------------------- Kakutani
+@pytest.mark.parametrize("tag", ["d20_m1", "d5_m2", "d360_m1"])
+def test_kakutani_points_bit_exact(P, golden, tag):
+    from paper_1408_5526_b200.samplers import DeviceSampler
+
+    g = golden("kakutani")
+    dim, m = int(tag[1:].split("_m")[0]), int(tag.split("_m")[1])
+    rows, ref = g[f"{tag}_rows"], g[f"{tag}_points"]
+    s = DeviceSampler("kakutani", dim, SEED, m)
+    pts = s.points(0, int(rows[-1]) + 1).cpu().numpy()
+    assert np.array_equal(pts[rows], ref)
+    k = rows.size // 2  # a single far row (snapshot start mid-stream)
+    assert np.array_equal(s.points(int(rows[k]), 1).cpu().numpy()[0], ref[k])
+
+
+def test_kakutani_fill_sequence(P, golden):
+    from paper_1408_5526_b200.samplers import DeviceSampler
+
+    g = golden("kakutani")
+    rows, ref = g["d5_m2_rows"], g["d5_m2_points"]
+    s = DeviceSampler("kakutani", 5, SEED, 2)
+    out = np.empty((50_000, 5))
+    for a, b in ((0, 1), (1, 8192), (8192, 8300), (8300, 50_000)):
+        s.fill(out[a:b])
+    sel = rows < 50_000
+    assert np.array_equal(out[rows[sel]], ref[sel])
+
+
+@pytest.mark.parametrize("tag,mk", [("libor20", "s20"), ("mbs", "mbs"), ("x1", "x1")])
+def test_kakutani_theta_vs_reference(P, golden, tag, mk):
+    g = golden("kakutani")
+    grid = tuple(int(n) for n in g[f"{tag}_grid"])
+    ref = g[f"{tag}_theta"]
+    cfg = P.ExperimentConfig(model=_model(mk).name, generator="kakutani", n_grid=grid,
+                             replications=ref.shape[1], seed=SEED)
+    rep = P.run_experiment(cfg, model=_model(mk))
+    got = np.stack([rep.estimates("kakutani", n) for n in grid])
+    if mk == "x1":
+        assert np.array_equal(got, ref)
+    else:
+        assert (np.abs(got / ref - 1)).max() <= THETA_RTOL
+
+
+def test_kakutani_theta_vs_oracle_large(P, oracle):
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    x1 = M.FirstCoordinateModel()
+    got = estimate_replications("kakutani", x1, SEED, 1, 3, (65_537, 700_001))
+    ref = oracle.run_replications("kakutani", x1, SEED, 1, 3, (65_537, 700_001), threads=3)
+    assert np.array_equal(got, ref)
+    lib = _model("s20")
+    got = estimate_replications("kakutani", lib, SEED, 2, 3, (200_003,))
+    ref = oracle.run_replications("kakutani", lib, SEED, 2, 3, (200_003,), threads=3)
+    assert (np.abs(got / ref - 1)).max() <= THETA_RTOL

@@ -281,3 +281,24 @@ def test_sequential_prng_estimates_bit_exact(oracle, golden, tag):
     mine = oracle.run_replications(gen, model, SEED, 1, theta.shape[1], t[f"{tag}_grid"],
                                    threads=4)
     assert np.array_equal(mine.T, theta)
+
+
+# ---------------------------------------------------------------- Kakutani
+def test_kakutani_points_bit_exact(oracle, golden):
+    g = golden("kakutani")
+    for tag in ("d20_m1", "d5_m2", "d360_m1"):
+        dim, m = int(tag[1:].split("_m")[0]), int(tag.split("_m")[1])
+        rows = g[f"{tag}_rows"]
+        key = oracle.derive_key(SEED, 6, m)
+        pts = oracle.kakutani_points(dim, key, int(rows[-1]) + 1)
+        assert np.array_equal(pts[rows], g[f"{tag}_points"]), tag
+
+
+def test_kakutani_estimates_bit_exact(oracle, golden):
+    g = golden("kakutani")
+    models = _golden_models(golden)
+    for tag, mk in (("libor20", "s20"), ("mbs", "mbs"), ("x1", "x1")):
+        theta = g[f"{tag}_theta"]
+        mine = oracle.run_replications("kakutani", models[mk], SEED, 1, theta.shape[1],
+                                       g[f"{tag}_grid"], threads=4)
+        assert np.array_equal(mine.T, theta), tag
