@@ -260,27 +260,6 @@ struct InvNormal {
   static constexpr double VSCALE = 0.16408352781008756;
 };
 
-RQ_HD double invn_central_num(double u) {
-  return ((((((-0.2919273214264852 * u + 9.193512285907598) * u + -62.454377324061355) * u +
-            170.0098658859532) * u + -211.46704297849197) * u + 113.93203453144044) * u +
-          -21.62514930947088) * u + 3.8841077977297096;
-}
-RQ_HD double invn_central_den(double u) {
-  return ((((((-0.4290780287479735 * u + 6.969736103714354) * u + -36.143835067804716) * u +
-            83.84882260510376) * u + -93.74669783914054) * u + 47.23127323999088) * u +
-          -8.96090814172393) * u + 1.5495348220676615;
-}
-RQ_HD double invn_tail_num(double w) {
-  return ((((((49.41588603624166 * w + 34.09554370467819) * w + -120.62391569766385) * w +
-            -36.11819081101896) * w + 77.35661807857605) * w + 12.678668433221901) * w +
-          -15.636790505919562) * w + -3.141967925161121;
-}
-RQ_HD double invn_tail_den(double w) {
-  return ((((((-0.0005317355830972598 * w + -8.101041244986659) * w + -2.3666362350675305) * w +
-            19.91298298968798) * w + -1.4094956335739925) * w + -10.941521790794202) * w +
-          1.2762506234112334) * w + 1.8704632131064214;
-}
-
 #if defined(__CUDACC__)
 // Fold p into the lower half: returns pl, sets *neg for p > 1/2.
 __device__ __forceinline__ double invn_fold(double p, bool *neg) {
@@ -303,22 +282,41 @@ __device__ __forceinline__ bool invn_tail_p(double p) {
 // q = fl(p - 1/2).  R is the reference rational in u = q^2 / R_MAX
 // (models.py:46-54) with the 1/R_MAX^k folded into the coefficients, so the
 // polynomials run directly in Q^2.
+// The coefficients live in the constant bank so every DFMA takes them as a
+// c[][] operand; as immediates ptxas materialises each double with two UMOVs
+// per use, which costs issue slots in the hot loops.
+__constant__ double c_invn_num[8] = {-18758.264827117993, 121493.75753172635, -169742.25554056765,
+                                     95028.92000917176,   -24309.66331940731, 2693.622228066229,
+                                     -105.1488511356405,  3.8841077977297096};
+__constant__ double c_invn_den[8] = {-27571.106587154845, 92106.19422816113, -98233.8844955836,
+                                     46868.23917353603,   -10776.85973982955, 1116.658786813825,
+                                     -43.57099147618938,  1.5495348220676615};
 __device__ __forceinline__ double invn_central_q(double Q) {
   const double s = Q * Q;
-  const double num =
-      ((((((-18758.264827117993 * s + 121493.75753172635) * s + -169742.25554056765) * s +
-          95028.92000917176) * s + -24309.66331940731) * s + 2693.622228066229) * s +
-       -105.1488511356405) * s + 3.8841077977297096;
-  const double den =
-      ((((((-27571.106587154845 * s + 92106.19422816113) * s + -98233.8844955836) * s +
-          46868.23917353603) * s + -10776.85973982955) * s + 1116.658786813825) * s +
-       -43.57099147618938) * s + 1.5495348220676615;
+  double num = c_invn_num[0], den = c_invn_den[0];
+#pragma unroll
+  for (int k = 1; k < 8; k++) {
+    num = fma(num, s, c_invn_num[k]);
+    den = fma(den, s, c_invn_den[k]);
+  }
   return div2(Q * num, den);
 }
 __device__ __forceinline__ double invn_central(double pl) { return invn_central_q(pl - 0.5); }
+__constant__ double c_invn_tnum[8] = {49.41588603624166,  34.09554370467819,  -120.62391569766385,
+                                      -36.11819081101896, 77.35661807857605,  12.678668433221901,
+                                      -15.636790505919562, -3.141967925161121};
+__constant__ double c_invn_tden[8] = {-0.0005317355830972598, -8.101041244986659, -2.3666362350675305,
+                                      19.91298298968798,       -1.4094956335739925, -10.941521790794202,
+                                      1.2762506234112334,      1.8704632131064214};
 __device__ __forceinline__ double invn_tail(double pl) {
-  double w = (sqrt(-2.0 * log(pl)) - InvNormal::VLO) * InvNormal::VSCALE;
-  return invn_tail_num(w) * rcp2(invn_tail_den(w));
+  const double w = (sqrt(-2.0 * log(pl)) - InvNormal::VLO) * InvNormal::VSCALE;
+  double num = c_invn_tnum[0], den = c_invn_tden[0];
+#pragma unroll
+  for (int k = 1; k < 8; k++) {
+    num = fma(num, w, c_invn_tnum[k]);
+    den = fma(den, w, c_invn_tden[k]);
+  }
+  return num * rcp2(den);
 }
 // Scalar Phi^-1 (divergent tail); the tile filler uses a compacted tail.
 __device__ __forceinline__ double inv_normal(double p) {

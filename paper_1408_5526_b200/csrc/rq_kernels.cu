@@ -1137,19 +1137,25 @@ struct ModelLibor {
 // and 3/4 above: |t| <= 0.1 for y in [0.381, 0.919] (MBS rates -1.2% ..
 // 4.2% at k3 = 10, k4 = 0.5) and the odd series to t^13 is exact to 7e-17;
 // other y: libdevice atan.
+__constant__ double c_atan_ser[6] = {0.07692307692307693, -0.09090909090909091,
+                                     0.1111111111111111,  -0.14285714285714285,
+                                     0.2,                 -0.3333333333333333};
+__constant__ double c_atan_ctr[4] = {0.5, 0.75, 0.4636476090008061, 0.6435011087932844};
+// range tests on the high word (ALU pipe, not a DSETP on the FP64 pipe);
+// they only choose between two valid evaluations, so they need not be exact
+__device__ __forceinline__ uint32_t abs_hi(double x) {
+  return (uint32_t)__double2hiint(x) & 0x7FFFFFFFu;
+}
 __device__ __forceinline__ double atan_mbs(double y) {
-  const bool hi = y >= 0.62;
-  const double c = hi ? 0.75 : 0.5;
+  const int hi = abs_hi(y) >= 0x3FE3D70Au;  // y >= ~0.62 (y > 0 here)
+  const double c = c_atan_ctr[hi];
   const double t = div2(y - c, fma(c, y, 1.0));
-  if (fabs(t) > 0.1) return atan(y);
+  if (abs_hi(t) > 0x3FB99999u || __double2hiint(y) < 0) return atan(y);  // |t| > ~0.1
   const double t2 = t * t;
-  double p = 0.07692307692307693;  // 1/13
-  p = fma(p, t2, -0.09090909090909091);
-  p = fma(p, t2, 0.1111111111111111);
-  p = fma(p, t2, -0.14285714285714285);
-  p = fma(p, t2, 0.2);
-  p = fma(p, t2, -0.3333333333333333);
-  return fma(t * t2, p, t) + (hi ? 0.6435011087932844 : 0.4636476090008061);
+  double p = c_atan_ser[0];
+#pragma unroll
+  for (int k = 1; k < 6; k++) p = fma(p, t2, c_atan_ser[k]);
+  return fma(t * t2, p, t) + c_atan_ctr[2 + hi];
 }
 
 // MBS present value (models.py:430-449), monthly steps.  State: discount
@@ -1163,7 +1169,8 @@ struct ModelMbs {
   using Shared = NoShared;
   static __host__ __device__ int gen_dims(int dim) { return dim; }
   const double *ck;
-  double i0, sxi, k0, k1, k2, k3, k4, pay, zlim;
+  double i0, sxi, k0, k1, k2, k3, k4, pay;
+  uint32_t zlim_hi;  // high word of exp_zlim: |z| below it stays in the series range
   double ec[MBS_EXP_TERMS];
   double disc, R, rate, omw, pv;
   __device__ void init(const ModelParams &mp_, Shared &) {
@@ -1176,7 +1183,7 @@ struct ModelMbs {
     k3 = mp_.k3;
     k4 = mp_.k4;
     pay = mp_.payment;
-    zlim = mp_.exp_zlim;
+    zlim_hi = abs_hi(mp_.exp_zlim);
 #pragma unroll
     for (int k = 0; k < MBS_EXP_TERMS; k++) ec[k] = mp_.ecoef[k];
   }
@@ -1188,7 +1195,7 @@ struct ModelMbs {
     pv = 0.0;
   }
   __device__ __forceinline__ double kexp(double z) const {  // k0 * exp(sigma_xi z)
-    if (fabs(z) > zlim) return k0 * exp(sxi * z);
+    if (abs_hi(z) >= zlim_hi) return k0 * exp(sxi * z);
     double p = ec[MBS_EXP_TERMS - 1];
 #pragma unroll
     for (int k = MBS_EXP_TERMS - 2; k >= 0; k--) p = fma(p, z, ec[k]);
