@@ -13,9 +13,12 @@
 //   model       thread-per-path state in registers (forward rates / MBS
 //               cash-flow state) advanced through the chunk's steps
 //
-// The generator of unit u+1 runs in the same iteration as normals+model of
-// unit u on the other half of a double-buffered tile, so the warps' uneven
-// generator work is absorbed by model work; one __syncthreads per unit.
+// Two CTA barriers per unit separate the phases; the 4-6 CTAs resident on an
+// SM are not in lock-step, so one CTA's generator phase overlaps another's
+// FP64-dense model phase.  (A double-buffered variant that generated unit
+// u+1 inside unit u's iteration measured slower and was dropped.)  The
+// generator's level buffers and the inverse normal's tail queue are never
+// live at the same time and share shared memory (PhaseShared).
 // The payoff (8 B/path) is the only HBM write; k_reduce then applies
 // numpy's pairwise-summation tree to each replication's payoff prefix
 // (bit-identical to the reference np.sum).
@@ -28,9 +31,6 @@
 #include "rq_device.cuh"
 #include "rq_internal.h"
 
-#ifndef RQ_PIPELINE
-#define RQ_PIPELINE 0  // 1: generate unit u+1 while modelling unit u (double-buffered tile)
-#endif
 #ifndef RQ_MINB_SMALL
 #define RQ_MINB_SMALL 4  // CTAs per SM targeted for LIBOR S <= 20 (register budget)
 #endif
@@ -158,7 +158,15 @@ __global__ void k_sobol_setup(RepTables t, const uint32_t *v, uint32_t *gen_v,
 // require path == base + threadIdx.x; "direct" ones take any index
 // (sampler.at).
 // ======================================================================
-constexpr int LEVBUF = 80;  // nodes per level buffer (>= TILE/2 + 2)
+constexpr int LEVBUF = 66;  // nodes per level buffer (>= TILE/2 + 2)
+
+// Shared memory of the phases that never overlap inside a unit: the
+// generator's per-warp ping-pong level buffers and the inverse normal's
+// per-warp tail queues.
+union PhaseShared {
+  double lev[WARPS][2][LEVBUF];
+  uint16_t tq[WARPS][CHUNK * 32];
+};
 
 constexpr int SIGD_MAX = 1024;  // sigma entries staged as doubles (single-chunk dims)
 
@@ -168,7 +176,6 @@ struct RasrapTileShared {
   int32_t J[CHUNK];                // top level (one node shared by the whole tile)
   int32_t hB[CHUNK];               // highest digit where B differs from n0 (-1: B == n0)
   double sJ[CHUNK];                // stream partial sum S_J of the top node
-  double lev[WARPS][2][LEVBUF];    // per-warp ping-pong level buffers
   int32_t st_rl[CHUNK];            // replication the state belongs to (-1: none)
   uint64_t st_base[CHUNK];         // tile base the state belongs to
   int32_t soff[CHUNK];             // offset of sigma_d in sigd
@@ -185,6 +192,20 @@ struct RasrapDirectShared {
 struct NoShared {
   int unused;
 };
+
+// kernels hand the phase-shared buffers to generators that use them
+template <class G>
+struct HasPhase {
+  template <class T>
+  static constexpr bool get(decltype(&T::ph)) { return true; }
+  template <class T>
+  static constexpr bool get(...) { return false; }
+  static constexpr bool value = get<G>(nullptr);
+};
+template <class G>
+__device__ __forceinline__ void give_phase(G &g, PhaseShared &p) {
+  if constexpr (HasPhase<G>::value) g.ph = &p;
+}
 
 // Recursive-form point at an arbitrary index (Alg. 2, halton.py:392-416)
 // without replaying the stream: for n = n0 + i let h be the highest digit
@@ -253,6 +274,7 @@ struct GenRasrapRecTile {
                                            RasrapTileShared>::type;
   const RepTables *t;
   Shared *sh;
+  PhaseShared *ph;  // level buffers (aliased with the tail queues, see PhaseShared)
   bool persist;   // consecutive tiles of one CTA share a persistent stream state
   bool sig_smem;  // sigma of the dims staged in shared memory as doubles
   __device__ void setup(const RepTables &t_, Shared &s, int gdims = 0) {
@@ -440,7 +462,7 @@ struct GenRasrapRecTile {
       const bool cw = h.sum_off + h.cap < CWTS;  // weights in the constant bank
       const double *w = g_wts + h.sum_off;
       const int J = R.J[dd], hB = R.hB[dd];
-      double *prev = R.lev[warp][0], *next = R.lev[warp][1];
+      double *prev = ph->lev[warp][0], *next = ph->lev[warp][1];
       if (lane == 0) prev[0] = R.sJ[dd];
       __syncwarp();
       // one node: S_j(prefix) = S_{j+1}(parent) + sigma(digit) * w_j, or the
@@ -1041,6 +1063,7 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc, uint16_t *q
 template <int S>
 struct ModelLibor {
   static constexpr bool NORMALS = true;
+  static constexpr bool SMALL_LIBOR = S <= 20;
   static constexpr int MINB = S <= 20 ? RQ_MINB_SMALL : (S <= 40 ? 3 : 2);  // CTAs/SM
   struct Shared {
     double l0[S];
@@ -1146,11 +1169,16 @@ __constant__ double c_atan_ctr[4] = {0.5, 0.75, 0.4636476090008061, 0.6435011087
 __device__ __forceinline__ uint32_t abs_hi(double x) {
   return (uint32_t)__double2hiint(x) & 0x7FFFFFFFu;
 }
+// out-of-range fallbacks: rare, kept out of line (instruction cache)
+__device__ __noinline__ double atan_slow(double y) { return atan(y); }
+__device__ __noinline__ double kexp_slow(double k0, double sxi, double z) {
+  return k0 * exp(sxi * z);
+}
 __device__ __forceinline__ double atan_mbs(double y) {
   const int hi = abs_hi(y) >= 0x3FE3D70Au;  // y >= ~0.62 (y > 0 here)
   const double c = c_atan_ctr[hi];
   const double t = div2(y - c, fma(c, y, 1.0));
-  if (abs_hi(t) > 0x3FB99999u || __double2hiint(y) < 0) return atan(y);  // |t| > ~0.1
+  if (abs_hi(t) > 0x3FB99999u || __double2hiint(y) < 0) return atan_slow(y);  // |t| > ~0.1
   const double t2 = t * t;
   double p = c_atan_ser[0];
 #pragma unroll
@@ -1164,7 +1192,8 @@ __device__ __forceinline__ double atan_mbs(double y) {
 // the reference's skipped update).
 struct ModelMbs {
   static constexpr bool NORMALS = true;
-  static constexpr int MINB = 4;
+  static constexpr bool SMALL_LIBOR = false;
+  static constexpr int MINB = 4;  // CTAs/SM (7 fit at <= 72 registers: measured 5% slower)
   static constexpr int MAXM = 1 << 20;
   using Shared = NoShared;
   static __host__ __device__ int gen_dims(int dim) { return dim; }
@@ -1195,7 +1224,7 @@ struct ModelMbs {
     pv = 0.0;
   }
   __device__ __forceinline__ double kexp(double z) const {  // k0 * exp(sigma_xi z)
-    if (abs_hi(z) >= zlim_hi) return k0 * exp(sxi * z);
+    if (abs_hi(z) >= zlim_hi) return kexp_slow(k0, sxi, z);
     double p = ec[MBS_EXP_TERMS - 1];
 #pragma unroll
     for (int k = MBS_EXP_TERMS - 2; k >= 0; k--) p = fma(p, z, ec[k]);
@@ -1249,6 +1278,7 @@ struct ModelMbs {
 template <bool CONST1>
 struct ModelTest {
   static constexpr bool NORMALS = false;
+  static constexpr bool SMALL_LIBOR = false;
   static constexpr int MINB = 4;
   using Shared = NoShared;
   static __host__ __device__ int gen_dims(int) { return CONST1 ? 0 : 1; }
@@ -1275,6 +1305,13 @@ struct PathArgs {
 
 constexpr size_t ZT_BYTES = sizeof(double) * CHUNK * TILE;  // one uniform/normal tile
 
+// CTAs/SM the launch bounds target: the model's choice, capped by the
+// generator's, except that the persistent Rasrap tile (shared-memory heavy,
+// generator phases latency bound) gains from a fifth CTA next to small LIBOR
+// (measured +1.7% at C2; Philox loses 3% at 5, so it stays at 4).
+template <class G, class Mdl>
+struct PathsMinB;
+
 template <class G>
 struct MaxBlocks {  // optional per-generator cap on CTAs/SM (register budget)
   template <class T>
@@ -1283,14 +1320,17 @@ struct MaxBlocks {  // optional per-generator cap on CTAs/SM (register budget)
   static constexpr int get(...) { return 8; }
   static constexpr int value = get<G>(nullptr);
 };
+template <class G, class Mdl>
+struct PathsMinB {
+  static constexpr int base = Mdl::MINB < MaxBlocks<G>::value ? Mdl::MINB : MaxBlocks<G>::value;
+  static constexpr int value =
+      std::is_same<G, GenRasrapRecTile<true>>::value && Mdl::SMALL_LIBOR ? 5 : base;
+};
 
 template <class G, class Mdl>
-__global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::MINB
-                                                                          : MaxBlocks<G>::value))
-    k_paths(PathArgs a) {
-  extern __shared__ __align__(16) double zdyn[];  // 2 x ZT_BYTES (double buffer)
-  auto zbuf = [&](int64_t u) { return zdyn + (u & 1) * (CHUNK * TILE); };
-  __shared__ uint16_t tq[WARPS][CHUNK * 32];
+__global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathArgs a) {
+  extern __shared__ __align__(16) double z[];  // ZT_BYTES
+  __shared__ PhaseShared phs;
   __shared__ typename G::Shared gsh;
   __shared__ typename Mdl::Shared msh;
   Mdl md;
@@ -1299,6 +1339,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
   const int gdims = Mdl::gen_dims(a.mp.dim);
   G g;
   g.setup(a.t, gsh, gdims);
+  give_phase(g, phs);
   __syncthreads();
   const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
   // tiles per launch <= (payoff batch 2^25 paths) / TILE: 32-bit counters
@@ -1334,26 +1375,15 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
   Cursor cur{a.rep_local0 + lo / tpr, 0, lo % tpr};
   auto dc_of = [&](int c) { return gdims - c * CHUNK < CHUNK ? gdims - c * CHUNK : CHUNK; };
   auto base_of = [&](const Cursor &q) { return (int64_t)q.tile * TILE; };
-  if (RQ_PIPELINE && gdims > 0)
-    g.unit(cur.rl, (uint64_t)base_of(cur), (uint64_t)(base_of(cur) + threadIdx.x), 0, dc_of(0),
-           zbuf(0));
-  __syncthreads();
   for (int u = 0; u < nunit; u++) {
-    Cursor nxt = cur;
-    advance(nxt);
     const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
     const int64_t base = base_of(cur);
-    double *z = zbuf(RQ_PIPELINE ? u : 0);
-    if (RQ_PIPELINE) {
-      if (gdims > 0 && u + 1 < nunit)  // generate the next unit into the other buffer
-        g.unit(nxt.rl, (uint64_t)base_of(nxt), (uint64_t)(base_of(nxt) + threadIdx.x),
-               nxt.c * CHUNK, dc_of(nxt.c), zbuf(u + 1));
-    } else if (gdims > 0) {
+    if (gdims > 0) {
       g.unit(rl, (uint64_t)base, (uint64_t)(base + threadIdx.x), d0, Dc, z);
       __syncthreads();
     }
     if (d0 == 0) md.begin();
-    if (Mdl::NORMALS) chunk_to_normals(z, Dc, tq[warp]);
+    if (Mdl::NORMALS) chunk_to_normals(z, Dc, phs.tq[warp]);
     md.chunk(d0, Dc, z + threadIdx.x);
     if (d0 + Dc >= gdims) {
       const int64_t path = base + threadIdx.x;
@@ -1361,7 +1391,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
         a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.payoff();
     }
     __syncthreads();
-    cur = nxt;
+    advance(cur);
   }
 }
 
@@ -1375,6 +1405,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
 // ======================================================================
 struct ModelPoints {  // sampler.fill of a sequential stream: write the uniforms
   static constexpr bool NORMALS = false;
+  static constexpr bool SMALL_LIBOR = false;
   static constexpr int MINB = 4;
   using Shared = NoShared;
   static __host__ __device__ int gen_dims(int dim) { return dim; }
@@ -1389,7 +1420,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
                                                                           : MaxBlocks<G>::value))
     k_paths_seq(PathArgs a, SeqArgs q) {
   extern __shared__ __align__(16) double z[];  // ZT_BYTES
-  __shared__ uint16_t tq[WARPS][CHUNK * 32];
+  __shared__ PhaseShared phs;
   __shared__ typename G::Shared gsh;
   __shared__ typename Mdl::Shared msh;
   constexpr bool POINTS = std::is_same<Mdl, ModelPoints>::value;
@@ -1433,7 +1464,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
             for (int dd = 0; dd < Dc; dd++)
               a.payoffs[off * dim + d0 + dd] = z[dd * TILE + threadIdx.x];
         } else {
-          if (Mdl::NORMALS) chunk_to_normals(z, Dc, tq[warp]);
+          if (Mdl::NORMALS) chunk_to_normals(z, Dc, phs.tq[warp]);
           md.chunk(d0, Dc, z + threadIdx.x);
           if (d0 + Dc >= gdims && ok)
             a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + off] = md.payoff();
@@ -1453,9 +1484,11 @@ __global__ void __launch_bounds__(TILE) k_points(RepTables t, int rl, int64_t fi
                                                  const int64_t *idx, int64_t count,
                                                  double *out) {
   extern __shared__ __align__(16) double zt[];  // ZT_BYTES
+  __shared__ PhaseShared phs;
   __shared__ typename G::Shared gsh;
   G g;
   g.setup(t, gsh, t.dim);
+  give_phase(g, phs);
   __syncthreads();
   for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < count; tb += (int64_t)gridDim.x * TILE) {
     const int64_t r = tb + threadIdx.x;
@@ -1480,11 +1513,12 @@ template <class G>
 __global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t npoints,
                                                  double *block_sums, double *store) {
   extern __shared__ __align__(16) double zt[];  // ZT_BYTES
-  __shared__ uint16_t tq[WARPS][CHUNK * 32];
+  __shared__ PhaseShared phs;
   __shared__ typename G::Shared gsh;
   __shared__ double red[WARPS];
   G g;
   g.setup(t, gsh, t.dim);
+  give_phase(g, phs);
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   double acc = 0.0;
@@ -1497,7 +1531,7 @@ __global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t np
       __syncthreads();
       g.unit(rl, (uint64_t)tb, (uint64_t)r, d0, Dc, zt);
       __syncthreads();
-      chunk_to_normals(zt, Dc, tq[warp]);
+      chunk_to_normals(zt, Dc, phs.tq[warp]);
       if (ok) {
         for (int dd = 0; dd < Dc; dd++) {
           double z = zt[dd * TILE + threadIdx.x];
@@ -1708,7 +1742,7 @@ template <class G, class Mdl>
 static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                             int *blocks_out) {
   const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
-  size_t dyn = prep_dyn(k_paths<G, Mdl>, (RQ_PIPELINE ? 2 : 1) * ZT_BYTES);
+  size_t dyn = prep_dyn(k_paths<G, Mdl>, ZT_BYTES);
   int blocks = persistent_blocks(k_paths<G, Mdl>, work, dyn);
   if (blocks_out) *blocks_out = blocks;
   if (probe) return cudaSuccess;
