@@ -943,7 +943,7 @@ int rq_stream_normals(rq_sampler *s, int32_t rep_local, int64_t npoints, double 
   if (rq::gen_sequential(s->t.gen))
     return fail(RQ_ERR_VALUE, "the normals stream is for counter/QMC generators (config 4)");
   cudaStream_t st = (cudaStream_t)stream;
-  int blocks = rq::paths_grid_blocks(s->t, rq::ModelParams{rq::MODEL_X1, s->t.dim});
+  int blocks = rq::stream_grid_blocks(s->t);
   double *bs = nullptr;
   RQ_CUDA(cudaMallocAsync((void **)&bs, sizeof(double) * blocks, st));
   RQ_CUDA(rq::launch_stream_normals(s->t, rep_local, npoints, bs, blocks, store_dev, st));

@@ -157,5 +157,6 @@ cudaError_t launch_stream_normals(const RepTables &t, int rep_local, int64_t npo
 cudaError_t launch_dfma_peak(int blocks, int iters, double *sink, cudaStream_t s);
 constexpr int PEAK_SLOTS_PER_ITER = 16 * 8;  // DFMA per thread per iteration of k_dfma_peak
 int paths_grid_blocks(const RepTables &t, const ModelParams &mp);
+int stream_grid_blocks(const RepTables &t);
 
 }  // namespace rq

@@ -561,6 +561,16 @@ struct GenPhilox {
       if (dd + 3 < Dc) zcol[(dd + 3) * TILE] = philox_u(w.w);
     }
   }
+  // register form for the normals stream: coordinates d0..d0+3 of `path`
+  __device__ __forceinline__ void quad(int rl, uint64_t path, int d0, double u[4]) {
+    const uint64_t key = derive_key3(t->seed, 3, (uint64_t)(t->rep_first + rl));
+    U4 w = philox4x32_10((uint32_t)(d0 >> 2), (uint32_t)path, (uint32_t)(path >> 32), 0u,
+                         (uint32_t)key, (uint32_t)(key >> 32));
+    u[0] = philox_u(w.x);
+    u[1] = philox_u(w.y);
+    u[2] = philox_u(w.z);
+    u[3] = philox_u(w.w);
+  }
 };
 
 // Scrambled Sobol' (sobol.py:313-372): the point at counter index j is the
@@ -645,6 +655,14 @@ struct GenSfc64 {
     }
     for (int dd = 0; dd < Dc; dd++)
       zt[dd * TILE + threadIdx.x] = (double)(sfc_next(s) >> 11) * TWO_M53;
+  }
+  __device__ __forceinline__ void quad(int rl, uint64_t path, int d0, double u[4]) {
+    if (d0 == 0) {
+      uint64_t km = derive_key3(t->seed, 7, (uint64_t)(t->rep_first + rl));
+      sfc_seed(s, splitmix64(km ^ path));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) u[k] = (double)(sfc_next(s) >> 11) * TWO_M53;
   }
 };
 
@@ -908,18 +926,18 @@ struct KakDim {
     b0 = b[0];
     b1 = b[1];
   }
+  // The reference's wrap test (x >= 1 after the step, halton.py:236-237)
+  // cannot fire in the first two brackets: k = 1 means 1 - x > 1/p + tol, so
+  // x + b_1 < 1; b_k < 0 for k >= 2.  Both candidates are formed before the
+  // bracket is known, which takes the compare off the latency chain.
   __device__ __forceinline__ double step(double x) const {
     const double om = 1.0 - x;
-    double v;
-    if (om > t0) {
-      v = x + b0;
-    } else if (om > t1) {
-      v = x + b1;
-    } else {
-      int k = 2;
-      while (k < KK_TAB - 1 && om <= thr[k]) k++;
-      v = x + b[k];
-    }
+    const double v0 = x + b0, v1 = x + b1;
+    if (om > t0) return v0;
+    if (om > t1) return v1;
+    int k = 2;
+    while (k < KK_TAB - 1 && om <= thr[k]) k++;
+    const double v = x + b[k];
     return v >= 1.0 ? v - 1.0 : v;
   }
 };
@@ -1551,6 +1569,79 @@ __global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t np
   }
 }
 
+// Register form of the stream for per-thread generators (Philox, SFC64):
+// four coordinates at a time straight from the generator into the central
+// inverse normal and the sum, no tile round trip through shared memory;
+// only the ~9% tail inputs go to a per-warp queue (value + store slot),
+// evaluated 32 at a time whenever 32 are waiting.
+template <class G>
+__global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_t npoints,
+                                                     double *block_sums, double *store) {
+  constexpr int QCAP = 32 + 4 * 32;  // < 32 left over + one 4-coordinate group
+  __shared__ double qv[WARPS][QCAP];
+  __shared__ int64_t qs[WARPS][QCAP];
+  __shared__ double red[WARPS];
+  __shared__ typename G::Shared gsh;
+  G g;
+  g.setup(t, gsh, t.dim);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  double acc = 0.0;
+  int qn = 0;
+  auto tail_one = [&](int i) {
+    bool neg;
+    const double x0 = invn_tail(invn_fold(qv[warp][i], &neg));
+    const double x = neg ? -x0 : x0;
+    acc += x;
+    if (store) store[qs[warp][i]] = x;
+  };
+  for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < npoints; tb += (int64_t)gridDim.x * TILE) {
+    const int64_t r = tb + threadIdx.x;
+    const bool ok = r < npoints;
+    for (int d0 = 0; d0 < t.dim; d0 += 4) {
+      double u[4], x[4];
+      bool tail[4], use[4];
+      g.quad(rl, (uint64_t)r, d0, u);
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        use[k] = ok && d0 + k < t.dim;
+        tail[k] = use[k] && invn_tail_p(u[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) x[k] = invn_central_q(u[k] - 0.5);
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if (use[k] && !tail[k]) {
+          acc += x[k];
+          if (store) store[r * t.dim + d0 + k] = x[k];
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, tail[k]);
+        if (tail[k]) {
+          const int i = qn + __popc(b & lt);
+          qv[warp][i] = u[k];
+          qs[warp][i] = r * t.dim + d0 + k;
+        }
+        qn += __popc(b);
+      }
+      __syncwarp();
+      while (qn >= 32) {
+        tail_one(qn - 32 + lane);
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+  }
+  if (lane < qn) tail_one(lane);
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sm = 0.0;
+    for (int k = 0; k < WARPS; k++) sm += red[k];
+    block_sums[blockIdx.x] = sm;
+  }
+}
+
 // ======================================================================
 // Model payoffs from caller uniforms (model.payoffs(u), models.py:311-322,
 // 462-469): thread per path, scalar inverse normal.
@@ -1969,6 +2060,18 @@ static cudaError_t stream_t(const RepTables &t, int rl, int64_t npoints, double 
   return cudaGetLastError();
 }
 
+int stream_grid_blocks(const RepTables &t) {
+  const int64_t big = (int64_t)1 << 30;
+  switch (t.gen) {
+    case GEN_PHILOX: return persistent_blocks(k_stream_reg<GenPhilox>, big);
+    case GEN_SFC64: return persistent_blocks(k_stream_reg<GenSfc64>, big);
+  }
+  ModelParams mp{};
+  mp.kind = MODEL_X1;
+  mp.dim = t.dim;
+  return paths_grid_blocks(t, mp);
+}
+
 cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
                                   double *block_sums, int nblocks, double *store,
                                   cudaStream_t s) {
@@ -1977,12 +2080,16 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
       return stream_t<GenRasrapRecTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_RASRAP_COUNTER:
       return stream_t<GenRasrapCounter>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_PHILOX: return stream_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_PHILOX:
+      k_stream_reg<GenPhilox><<<nblocks, TILE, 0, s>>>(t, rl, npoints, block_sums, store);
+      return cudaGetLastError();
     case GEN_SOBOL_GRAY:
       return stream_t<GenSobolTile<true>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_SOBOL_COUNTER:
       return stream_t<GenSobolTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_SFC64: return stream_t<GenSfc64>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_SFC64:
+      k_stream_reg<GenSfc64><<<nblocks, TILE, 0, s>>>(t, rl, npoints, block_sums, store);
+      return cudaGetLastError();
   }
   return cudaErrorInvalidValue;
 }
