@@ -66,7 +66,7 @@ def traffic_per_launch(workload: str, gen: str, M: int, N: int):
         bpp = tab[f"{workload}/{gen}"]["dram_bytes_per_path"]
     except (OSError, KeyError, ValueError):
         return None
-    per_launch = min(M, max(1, (32 << 20) // N)) * N  # rq_estimate's replication batch
+    per_launch = min(M, max(1, (128 << 20) // N)) * N  # rq_estimate's replication batch
     return bpp * per_launch
 
 

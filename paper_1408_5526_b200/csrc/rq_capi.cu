@@ -824,8 +824,8 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
   double *tab = nullptr;
   if ((rc = model_to_params(model, s->t.dim, mp, &tab, st))) return rc;
   const int64_t nmax = grid_host[ngrid - 1];
-  // replication batch: payoff buffer <= 256 MiB, >= 1 replication
-  int64_t B = std::max<int64_t>(1, ((int64_t)32 << 20) / nmax);
+  // replication batch: payoff buffer <= 1 GiB (2^27 paths), >= 1 replication
+  int64_t B = std::max<int64_t>(1, ((int64_t)128 << 20) / nmax);
   B = std::min<int64_t>(B, s->t.rep_count);
   std::vector<HostPlan> hplans(ngrid);
   std::vector<DevPlan> dplans(ngrid);

@@ -1360,7 +1360,7 @@ __global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathAr
   give_phase(g, phs);
   __syncthreads();
   const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
-  // tiles per launch <= (payoff batch 2^25 paths) / TILE: 32-bit counters
+  // tiles per launch <= (payoff batch 2^27 paths) / TILE: 32-bit counters
   const int total = a.rep_n * (int)a.tiles_per_rep;
   if ((int)blockIdx.x >= total) return;
   // Single-chunk models: CTA b owns the contiguous tiles [lo, hi) of the
