@@ -31,6 +31,9 @@
 #include "rq_device.cuh"
 #include "rq_internal.h"
 
+#ifndef RQ_MBS_MG
+#define RQ_MBS_MG 4  // MBS months evaluated together (ILP across months)
+#endif
 #ifndef RQ_MINB_SMALL
 #define RQ_MINB_SMALL 4  // CTAs per SM targeted for LIBOR S <= 20 (register budget)
 #endif
@@ -1193,15 +1196,15 @@ __device__ __noinline__ double kexp_slow(double k0, double sxi, double z) {
   return k0 * exp(sxi * z);
 }
 __device__ __forceinline__ double atan_mbs(double y) {
-  const int hi = abs_hi(y) >= 0x3FE3D70Au;  // y >= ~0.62 (y > 0 here)
-  const double c = c_atan_ctr[hi];
+  const bool hi = abs_hi(y) >= 0x3FE3D70Au;  // y >= ~0.62 (y > 0 here)
+  const double c = hi ? c_atan_ctr[1] : c_atan_ctr[0];
   const double t = div2(y - c, fma(c, y, 1.0));
   if (abs_hi(t) > 0x3FB99999u || __double2hiint(y) < 0) return atan_slow(y);  // |t| > ~0.1
   const double t2 = t * t;
   double p = c_atan_ser[0];
 #pragma unroll
   for (int k = 1; k < 6; k++) p = fma(p, t2, c_atan_ser[k]);
-  return fma(t * t2, p, t) + c_atan_ctr[2 + hi];
+  return fma(t * t2, p, t) + (hi ? c_atan_ctr[3] : c_atan_ctr[2]);
 }
 
 // MBS present value (models.py:430-449), monthly steps.  State: discount
@@ -1252,7 +1255,7 @@ struct ModelMbs {
   // reciprocals and the prepayment arctangents of a group are independent
   // once the (cheap, serial) rate product is known, so they are issued
   // together; only disc / R / pv remain serial (models.py:437-448).
-  static constexpr int MG = 4;
+  static constexpr int MG = RQ_MBS_MG;
   __device__ void chunk(int d0, int Dc, const double *zcol) {
     int kk = 0;
     for (; kk + MG <= Dc; kk += MG) {
