@@ -658,12 +658,14 @@ static int seq_begin(const rq::RepTables &t, const rq::ModelParams &mp, int B, i
   int segs;
   rq::seq_layout(t, mp, B, nmax, &L, &segs, &R.ctas);
   R.q.p0 = p0;
+  R.q.nmax = nmax;
   R.q.seg_len = L;
   R.q.segs_per_rep = segs;
   if (t.gen == rq::GEN_XORWOW) return RQ_OK;
   const bool mt = t.gen == rq::GEN_TWISTER;
   const size_t per_rep = mt ? sizeof(uint32_t) * rq::MT_N * (size_t)segs
-                            : sizeof(double) * t.dim * (size_t)segs;
+                            : sizeof(double) * t.dim * (size_t)segs *
+                                  (rq::kak_runs(t.dim) ? 128 : 1);
   int64_t G = std::max<int64_t>(B, ((int64_t)256 << 20) / (int64_t)per_rep / B * B);
   G = std::min<int64_t>(G, t.rep_count);
   R.grp_cap = G;

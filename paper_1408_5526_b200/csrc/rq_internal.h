@@ -88,11 +88,13 @@ struct RepTables {
 // paths and jumps its own state there with precomputed matrix powers.
 struct SeqArgs {
   int64_t p0;          // first path of the range (sampler.fill cursor; 0 for estimates)
+  int64_t nmax;        // paths in the range
   int64_t seg_len;     // paths per segment (multiple of the tile)
   int32_t segs_per_rep;
   const uint32_t *mt_snap;  // [rep - rep_local0][seg][MT_N] raw MT state after the twist that
                             // produced the segment's first word
-  const double *kk_snap;    // [rep - rep_local0][seg][dim] Kakutani orbit points at segment starts
+  const double *kk_snap;    // Kakutani orbit points at segment starts, [rep - rep_local0][seg][dim]
+                            // (tile layout) or at run starts, [rep - rep_local0][seg][TILE][dim]
   uint32_t *scratch;        // [gridDim][dim][TILE] tempered MT words (Kakutani: doubles) of a tile
 };
 
@@ -136,6 +138,8 @@ cudaError_t upload_kakutani_tables(const double *thr, const double *b, int dims)
 cudaError_t launch_kakutani_setup(const RepTables &t, double *x0, cudaStream_t s);
 cudaError_t launch_kak_snap(const RepTables &t, int rep_local0, int rep_n, const SeqArgs &q,
                             double *snap, cudaStream_t s);
+constexpr int KK_RUNS_MAXDIM = 40;  // Kakutani: per-thread runs (orbit state in smem) up to this dim
+__host__ __device__ constexpr bool kak_runs(int dim) { return dim <= KK_RUNS_MAXDIM; }
 cudaError_t launch_xorwow_setup(const RepTables &t, uint32_t *state, cudaStream_t s);
 // choose the segment length / grid of the sequential-stream path kernel
 void seq_layout(const RepTables &t, const ModelParams &mp, int rep_n, int64_t nmax,

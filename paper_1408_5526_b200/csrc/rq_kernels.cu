@@ -711,6 +711,8 @@ __global__ void k_xorwow_setup(RepTables t, uint32_t *state) {
 // of the xorshift part for the set bits of W (the Weyl counter d advances
 // by 362437 W).
 struct GenXorwow {
+  __device__ void set_dyn(double *) {}
+  static __host__ __device__ size_t dyn_bytes(int) { return 0; }
   static constexpr bool RUNS = true;
   using Shared = NoShared;
   const RepTables *t;
@@ -839,6 +841,8 @@ __global__ void __launch_bounds__(256) k_mt_snap(RepTables t, int rep_local0, in
 // paths, twists and tempers the tile's words (path-major) into a per-CTA
 // scratch laid out [dim][TILE], from which every thread reads its path.
 struct GenTwister {
+  __device__ void set_dyn(double *) {}
+  static __host__ __device__ size_t dyn_bytes(int) { return 0; }
   static constexpr bool RUNS = false;
   struct Shared {
     uint32_t st[2][MT_N];
@@ -910,38 +914,98 @@ struct GenTwister {
 __device__ double g_kk_thr[MAX_DIM * KK_TAB];
 __device__ double g_kk_b[MAX_DIM * KK_TAB];
 
+// cached brackets of the bases of the runs layout, [dim][thr 0..7, b 0..7]:
+// warp-uniform reads from the constant bank
+__constant__ double c_kk8[KK_RUNS_MAXDIM * 16];
+
 cudaError_t upload_kakutani_tables(const double *thr, const double *b, int dims) {
   cudaError_t e = cudaMemcpyToSymbol(g_kk_thr, thr, sizeof(double) * dims * KK_TAB);
   if (e != cudaSuccess) return e;
-  return cudaMemcpyToSymbol(g_kk_b, b, sizeof(double) * dims * KK_TAB);
+  e = cudaMemcpyToSymbol(g_kk_b, b, sizeof(double) * dims * KK_TAB);
+  if (e != cudaSuccess) return e;
+  double c8[KK_RUNS_MAXDIM * 16];
+  const int nd = dims < KK_RUNS_MAXDIM ? dims : KK_RUNS_MAXDIM;
+  for (int d = 0; d < nd; d++)
+    for (int j = 0; j < 8; j++) {
+      c8[d * 16 + j] = thr[d * KK_TAB + j];
+      c8[d * 16 + 8 + j] = b[d * KK_TAB + j];
+    }
+  return cudaMemcpyToSymbol(c_kk8, c8, sizeof(double) * 16 * nd);
 }
 
 // One orbit step, the first two brackets (probability 1 - 1/p^2) in
 // registers, off the L1 latency chain of the sequential orbit.
-struct KakDim {
-  const double *thr, *b;
-  double t0, t1, b0, b1;
-  __device__ void load(int d) {
-    thr = g_kk_thr + d * KK_TAB;
-    b = g_kk_b + d * KK_TAB;
-    t0 = thr[0];
-    t1 = thr[1];
-    b0 = b[0];
-    b1 = b[1];
+constexpr int KK_NB = 8;  // brackets held in registers / the constant bank
+// One orbit step from cached brackets tc/bc (k < KK_NB) and the global
+// tables beyond.  The reference's wrap test (x >= 1 after the step,
+// halton.py:236-237) cannot fire in the cached brackets: k = 1 means
+// 1 - x > 1/p + tol, so x + b_1 < 1, and b_k < 0 for k >= 2.  The first two
+// candidates are formed before the bracket is known (off the latency chain);
+// deeper brackets (probability 1/p^2) are found by an unrolled scan.
+template <class TC, class BC>
+__device__ __forceinline__ double kak_step(double x, TC tc, BC bc, const double *thr,
+                                           const double *b) {
+  const double om = 1.0 - x;
+  const double v0 = x + bc(0), v1 = x + bc(1);
+  if (om > tc(0)) return v0;
+  if (om > tc(1)) return v1;
+  double v = 0.0;
+  bool found = false;
+#pragma unroll
+  for (int j = 2; j < KK_NB; j++) {
+    if (!found && om > tc(j)) {
+      v = x + bc(j);
+      found = true;
+    }
   }
-  // The reference's wrap test (x >= 1 after the step, halton.py:236-237)
-  // cannot fire in the first two brackets: k = 1 means 1 - x > 1/p + tol, so
-  // x + b_1 < 1; b_k < 0 for k >= 2.  Both candidates are formed before the
-  // bracket is known, which takes the compare off the latency chain.
-  __device__ __forceinline__ double step(double x) const {
-    const double om = 1.0 - x;
-    const double v0 = x + b0, v1 = x + b1;
-    if (om > t0) return v0;
-    if (om > t1) return v1;
-    int k = 2;
+  if (!found) {
+    int k = KK_NB;
+    while (k < KK_TAB - 1 && om <= thr[k]) k++;
+    v = x + b[k];
+    v = v >= 1.0 ? v - 1.0 : v;
+  }
+  return v;
+}
+
+// Branch-free form for the latency-bound snapshot walks (a warp holds
+// orbits of different bases, so the branchy form diverges every step):
+// the bracket is the number of cached thresholds >= 1 - x (they decrease),
+// the increment is picked by a select tree on its bits.
+__device__ __forceinline__ double kak_step_flat(double x, const double *tc, const double *bc,
+                                                const double *thr, const double *b) {
+  const double om = 1.0 - x;
+  int k = 0;
+#pragma unroll
+  for (int j = 0; j < KK_NB; j++) k += om <= tc[j] ? 1 : 0;
+  if (k == KK_NB) {  // deeper than the cache: rare
     while (k < KK_TAB - 1 && om <= thr[k]) k++;
     const double v = x + b[k];
     return v >= 1.0 ? v - 1.0 : v;
+  }
+  const double s01 = (k & 1) ? bc[1] : bc[0], s23 = (k & 1) ? bc[3] : bc[2];
+  const double s45 = (k & 1) ? bc[5] : bc[4], s67 = (k & 1) ? bc[7] : bc[6];
+  const double s03 = (k & 2) ? s23 : s01, s47 = (k & 2) ? s67 : s45;
+  return x + ((k & 4) ? s47 : s03);
+}
+
+struct KakDim {  // one base's brackets in registers
+  const double *thr, *b;
+  double tc[KK_NB], bc[KK_NB];
+  __device__ void load(int d) {
+    thr = g_kk_thr + d * KK_TAB;
+    b = g_kk_b + d * KK_TAB;
+#pragma unroll
+    for (int j = 0; j < KK_NB; j++) {
+      tc[j] = thr[j];
+      bc[j] = b[j];
+    }
+  }
+  __device__ __forceinline__ double step(double x) const {
+    return kak_step(
+        x, [&](int j) { return tc[j]; }, [&](int j) { return bc[j]; }, thr, b);
+  }
+  __device__ __forceinline__ double step_flat(double x) const {
+    return kak_step_flat(x, tc, bc, thr, b);
   }
 };
 
@@ -970,15 +1034,87 @@ __global__ void k_kak_snap(RepTables t, int rep_local0, int rep_n, SeqArgs q, do
   for (int sg = 0; sg < q.segs_per_rep; sg++) {
     const int64_t P = q.p0 + (int64_t)sg * q.seg_len;
 #pragma unroll 4
-    for (; pos < P; pos++) x = kd.step(x);
+    for (; pos < P; pos++) x = kd.step_flat(x);
     snap[((int64_t)rb * q.segs_per_rep + sg) * t.dim + d] = x;
   }
 }
+
+// Orbit points at the run starts of every segment (the per-thread runs
+// layout): P = p0 + s seg_len + t ntile_s, t < TILE.
+__global__ void k_kak_snap_runs(RepTables t, int rep_local0, int rep_n, SeqArgs q,
+                                double *snap) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)rep_n * t.dim) return;
+  const int rb = (int)(gid / t.dim), d = (int)(gid % t.dim);
+  KakDim kd;
+  kd.load(d);
+  double x = t.kk_x0[(int64_t)(rep_local0 + rb) * t.dim + d];
+  int64_t pos = 0;
+  for (int sg = 0; sg < q.segs_per_rep; sg++) {
+    const int64_t s0 = (int64_t)sg * q.seg_len;
+    const int64_t slen = q.seg_len < q.nmax - s0 ? q.seg_len : q.nmax - s0;
+    const int64_t ntile = (slen + TILE - 1) / TILE;
+    for (int tt = 0; tt < TILE; tt++) {
+      int64_t P = q.p0 + s0 + (int64_t)tt * ntile;
+      if (P > q.p0 + s0 + slen) P = q.p0 + s0 + slen;  // empty run: never read
+#pragma unroll 4
+      for (; pos < P; pos++) x = kd.step_flat(x);
+      snap[(((int64_t)rb * q.segs_per_rep + sg) * TILE + tt) * t.dim + d] = x;
+    }
+  }
+}
+
+// Per-thread runs (dim <= KK_RUNS_MAXDIM): thread t owns paths
+// [t ntile, (t+1) ntile) of a segment and steps each dimension's orbit once
+// per path, the orbit values of its dims in the dynamic shared memory
+// xs[dim][TILE] next to the tile; the dims' first brackets come from the
+// constant bank (warp-uniform).  No barrier and no idle thread in the walk.
+struct GenKakutaniRuns {
+  static constexpr bool RUNS = true;
+  using Shared = NoShared;
+  const RepTables *t;
+  const SeqArgs *q;
+  double *xs;
+  int dim;
+  __device__ void setup(const RepTables &t_, Shared &, uint32_t *) { t = &t_; }
+  __device__ void set_seq(const SeqArgs &q_, int dim_) {
+    q = &q_;
+    dim = dim_;
+  }
+  __device__ void set_dyn(double *p) { xs = p; }
+  static __host__ __device__ size_t dyn_bytes(int dim_) { return sizeof(double) * dim_ * TILE; }
+  __device__ __forceinline__ double step(int d, double x) const {
+    const double *c = c_kk8 + d * 16;
+    return kak_step(
+        x, [&](int j) { return c[j]; }, [&](int j) { return c[8 + j]; },
+        g_kk_thr + d * KK_TAB, g_kk_b + d * KK_TAB);
+  }
+  __device__ void begin_segment(int, int rb, int sg, int64_t, int64_t, int) {
+    const double *src = q->kk_snap + (((int64_t)rb * q->segs_per_rep + sg) * TILE + threadIdx.x) * dim;
+    for (int d = 0; d < dim; d++) xs[d * TILE + threadIdx.x] = src[d];
+  }
+  __device__ void unit(int, int, int d0, int Dc, double *zt) {
+    for (int dd = 0; dd < Dc; dd++) {
+      double *xp = xs + (d0 + dd) * TILE + threadIdx.x;
+      const double x = *xp;
+      zt[dd * TILE + threadIdx.x] = x;
+      *xp = step(d0 + dd, x);
+    }
+  }
+  __device__ void skip(int n) {  // the dims a path-free model does not read
+    for (int d = dim - n; d < dim; d++) {
+      double *xp = xs + d * TILE + threadIdx.x;
+      *xp = step(d, *xp);
+    }
+  }
+};
 
 // Tile layout (TILE consecutive paths): at chunk 0 of a tile, thread t
 // advances the orbits of dims t, t + TILE, ... over the tile's paths into
 // the per-CTA scratch [dim][TILE] (doubles); chunks read their columns.
 struct GenKakutani {
+  __device__ void set_dyn(double *) {}
+  static __host__ __device__ size_t dyn_bytes(int) { return 0; }
   static constexpr bool RUNS = false;
   struct Shared {
     double xs[MAX_DIM];  // orbit state of every dim between tiles
@@ -1452,7 +1588,8 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
   const int gdims = Mdl::gen_dims(dim);
   G g;
   g.setup(a.t, gsh, q.scratch + (size_t)blockIdx.x * dim * TILE);
-  if constexpr (!G::RUNS) g.set_seq(q, dim);
+  if constexpr (!G::RUNS || std::is_same<G, GenKakutaniRuns>::value) g.set_seq(q, dim);
+  g.set_dyn(z + CHUNK * TILE);
   __syncthreads();
   const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
   const int64_t nunits = (int64_t)a.rep_n * q.segs_per_rep;
@@ -1921,7 +2058,11 @@ cudaError_t launch_kakutani_setup(const RepTables &t, double *x0, cudaStream_t s
 cudaError_t launch_kak_snap(const RepTables &t, int rep_local0, int rep_n, const SeqArgs &q,
                             double *snap, cudaStream_t s) {
   const int64_t n = (int64_t)rep_n * t.dim;
-  k_kak_snap<<<(int)((n + 127) / 128), 128, 0, s>>>(t, rep_local0, rep_n, q, snap);
+  // latency-bound sequential walks: small CTAs spread them over all SMs
+  if (kak_runs(t.dim))
+    k_kak_snap_runs<<<(int)((n + 31) / 32), 32, 0, s>>>(t, rep_local0, rep_n, q, snap);
+  else
+    k_kak_snap<<<(int)((n + 31) / 32), 32, 0, s>>>(t, rep_local0, rep_n, q, snap);
   return cudaGetLastError();
 }
 
@@ -1934,7 +2075,7 @@ cudaError_t launch_mt_snap(const RepTables &t, int rep_local0, int rep_n, const 
 template <class G, class Mdl>
 static cudaError_t seq_gm(const PathArgs &a, const SeqArgs &q, int blocks, int *launched,
                           cudaStream_t s, int *occ) {
-  size_t dyn = prep_dyn(k_paths_seq<G, Mdl>, ZT_BYTES);
+  size_t dyn = prep_dyn(k_paths_seq<G, Mdl>, ZT_BYTES + G::dyn_bytes(a.mp.dim));
   if (occ) {
     *occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_paths_seq<G, Mdl>, TILE, dyn);
@@ -1972,7 +2113,9 @@ static cudaError_t seq_dispatch(const PathArgs &a, const SeqArgs &q, int blocks,
   switch (a.t.gen) {
     case GEN_TWISTER: return seq_g<GenTwister>(a, q, blocks, launched, s, occ);
     case GEN_XORWOW: return seq_g<GenXorwow>(a, q, blocks, launched, s, occ);
-    case GEN_KAKUTANI: return seq_g<GenKakutani>(a, q, blocks, launched, s, occ);
+    case GEN_KAKUTANI:
+      return kak_runs(a.t.dim) ? seq_g<GenKakutaniRuns>(a, q, blocks, launched, s, occ)
+                               : seq_g<GenKakutani>(a, q, blocks, launched, s, occ);
   }
   return cudaErrorInvalidValue;
 }
