@@ -349,10 +349,38 @@ def run_ours(args) -> dict:
         }
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(model, gen, N, args)
+        if args.workload == "c2" and not use_dist and not args.reps:
+            out["comparison"] = generator_comparison(model, M, N)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return out
+
+
+def generator_comparison(model, M: int, N: int) -> dict:
+    """Config 2's comparison (BASELINE configs[1]): random-start Halton vs
+    Philox MC vs scrambled Sobol' on the same caplet, M x N, through the
+    host API.  Standard error SE = std(theta) / sqrt(M); the reference's
+    efficiency column is std x seconds per replication (harness.py:364-385);
+    variance reduction = (SE_philox / SE)^2 at equal N."""
+    import numpy as np
+
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    res = {}
+    for g in ("rasrap-recursive", "philox", "sobol-gray"):
+        estimate_replications(g, model, SEED, 1, 2, (N,))  # warm
+        t0 = time.perf_counter()
+        th = estimate_replications(g, model, SEED, 1, M, (N,))[:, 0]
+        sec = time.perf_counter() - t0
+        std = float(np.std(th, ddof=1))
+        res[g] = {"paths_per_s": M * N / sec, "mean": float(th.mean()),
+                  "std_error": std / math.sqrt(M), "efficiency_std_x_s": std * sec / M,
+                  "std_error_per_s": std / math.sqrt(M) / sec}
+    base = res["philox"]["std_error"]
+    for g in res:
+        res[g]["variance_reduction_vs_philox"] = (base / res[g]["std_error"]) ** 2
+    return {"workload": f"LIBOR S={model.dim}, M={M} x N={N}, seed {SEED}", "generators": res}
 
 
 # ---------------------------------------------------------------- reference arm
