@@ -132,6 +132,8 @@ const HostTables &host_tables() {
       unsigned __int128 M = ((((unsigned __int128)1) << (46 + ell)) + p - 1) / p;
       h.m64 = (uint64_t)(M << (18 - ell));
       h.m16 = (uint32_t)(((((uint64_t)1) << 32) + p - 1) / p);  // ceil(2^32/p)
+      h.tdig = 0;
+      for (int v = 128 / p; v > 0; v /= p) h.tdig++;  // 128 = the device tile (TILE)
       h.sig_off = sig;
       h.dig_off = dig;
       h.sum_off = sum;

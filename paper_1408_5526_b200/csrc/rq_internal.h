@@ -52,7 +52,7 @@ struct HaltonDim {
   int32_t sum_off;  // offset of partial sums / weight tables (sum of cap+1)
   uint64_t m64;     // floor(x / base) = umulhi64(x, m64) for x < 2^46
   uint32_t m16;     // floor(x / base) = umulhi(x, m16) for x < 2^16
-  uint32_t pad_;
+  int32_t tdig;     // highest nonzero base-p digit position of the tile size (128)
   double inv_p;     // 1.0 / base
   double scale0;    // Python pow(inv_p, K): first init-sum weight (halton.py:274)
 };

@@ -325,12 +325,12 @@ struct GenRasrapRecTile {
   // Odometer step B -> B + TILE (the adding machine on the digit vector):
   // add TILE's base-p digits with carry, then re-chain the partial sums
   // below the highest changed digit.
-  __device__ void state_advance(int rl, int d, int dd) {
+  // Odometer step B -> B + TILE on the digits; returns the highest changed
+  // digit (>= h.tdig: the top digit of TILE changes or carries out).
+  __device__ int digits_advance(int d, int dd) {
     Shared &R = *sh;
     const HaltonDim &h = c_hdim[d];
     const uint32_t p = (uint32_t)h.base;
-    const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
-    const double *w = g_wts + h.sum_off;
     uint32_t r = TILE, carry = 0;
     int j = 0, jmax = -1;
 #pragma unroll 1
@@ -346,13 +346,24 @@ struct GenRasrapRecTile {
       j++;
     }
     int hB = R.hB[dd];
-    hB = jmax > hB ? jmax : hB;  // a carry above hB makes that digit exceed n0's
-    R.hB[dd] = hB;
+    R.hB[dd] = jmax > hB ? jmax : hB;  // a carry above hB makes that digit exceed n0's
+    return jmax;
+  }
+  // Re-chain the partial sums P[k] = S_k(B) for k = jmax .. kmin.  Only
+  // P[J] (this tile's top node) and P[k > tdig] (where every later re-chain
+  // starts, since its jmax >= tdig) are ever read again, so the chain stops
+  // at kmin = min(J, tdig + 1) instead of 0; P[k < kmin] go stale unused.
+  __device__ void rechain(int rl, int d, int dd, int jmax, int kmin) {
+    Shared &R = *sh;
+    const HaltonDim &h = c_hdim[d];
+    const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
+    const double *w = g_wts + h.sum_off;
+    const int hB = R.hB[dd];
     double S = R.P[dd][jmax + 1];
     const double *sgd = sigd_of(dd);
     const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
 #pragma unroll 1
-    for (int k = jmax; k >= 0; k--) {
+    for (int k = jmax; k >= kmin; k--) {
       const double sv = sig_smem ? sgd[R.bd[dd][k]] : u16d(sg[R.bd[dd][k]]);
       S = k > hB ? ini[k] : dadd(S, dmul(sv, w[k]));
       R.P[dd][k] = S;
@@ -371,11 +382,9 @@ struct GenRasrapRecTile {
       return;
     }
     if constexpr (PERSIST) {
-      if (R.st_rl[dd] == rl && R.st_base[dd] + TILE == base) {
-        state_advance(rl, d, dd);
-      } else {
-        state_full(rl, base, d, dd);
-      }
+      const bool adv = R.st_rl[dd] == rl && R.st_base[dd] + TILE == base;
+      const int jmax = adv ? digits_advance(d, dd) : -1;
+      if (!adv) state_full(rl, base, d, dd);
       R.st_rl[dd] = rl;
       R.st_base[dd] = base;
       int N = TILE, J = 0;
@@ -386,6 +395,7 @@ struct GenRasrapRecTile {
         J++;
         R.nn[dd][J] = (int16_t)N;
       }
+      if (adv) rechain(rl, d, dd, jmax, J < h.tdig + 1 ? J : h.tdig + 1);
       R.J[dd] = J;
       R.sJ[dd] = sh->P[dd][J];
     }
