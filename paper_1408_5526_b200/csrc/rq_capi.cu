@@ -641,7 +641,7 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
 // Sequential streams: segment layout, MT19937 snapshots and the per-CTA
 // word scratch for paths [p0, p0 + nmax) of batches of <= B replications.
 // The snapshot walk is sequential per replication (latency bound), so it is
-// launched for a whole group of batches at once (<= 256 MiB of snapshots).
+// launched for a whole group of batches at once (<= 1 GiB of snapshots).
 struct SeqRun {
   rq::SeqArgs q{};
   int ctas = 0;
@@ -668,7 +668,9 @@ static int seq_begin(const rq::RepTables &t, const rq::ModelParams &mp, int B, i
   const size_t per_rep = mt ? sizeof(uint32_t) * rq::MT_N * (size_t)segs
                             : sizeof(double) * t.dim * (size_t)segs *
                                   (rq::kak_runs(t.dim) ? 128 : 1);
-  int64_t G = std::max<int64_t>(B, ((int64_t)256 << 20) / (int64_t)per_rep / B * B);
+  // the walk is latency bound (its time hardly depends on the group size):
+  // few, large groups (<= 1 GiB of snapshots)
+  int64_t G = std::max<int64_t>(B, ((int64_t)1024 << 20) / (int64_t)per_rep / B * B);
   G = std::min<int64_t>(G, t.rep_count);
   R.grp_cap = G;
   size_t b_scr = (mt ? sizeof(uint32_t) : sizeof(double)) * (size_t)R.ctas * t.dim * 128;

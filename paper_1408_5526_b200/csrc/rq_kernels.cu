@@ -49,6 +49,7 @@ constexpr double TWO_M53 = 1.1102230246251565e-16;  // 2^-53
 
 __constant__ HaltonDim c_hdim[MAX_DIM];
 constexpr int CWTS = 1280;  // binpow weights of the first dims, in the constant bank
+static_assert(CHUNK_DIMS <= 40, "persistent Rasrap tiles assume their weights fit c_wts");
 __constant__ double c_wts[CWTS];
 constexpr int WTS_CAP = 16384;
 __device__ double g_wts[WTS_CAP];     // binpow(inv_p, j+1): numba `x ** int` (halton.py:409)
@@ -472,7 +473,9 @@ struct GenRasrapRecTile {
       const uint16_t *sg = gsig + h.sig_off;
       const double *sgd = sigd_of(dd);
       const double *ini = gsum + h.sum_off;
-      const bool cw = h.sum_off + h.cap < CWTS;  // weights in the constant bank
+      // weights in the constant bank (always so for a persistent single-chunk
+      // model: its <= CHUNK dims use < CWTS weights)
+      const bool cw = PERSIST || h.sum_off + h.cap < CWTS;
       const double *w = g_wts + h.sum_off;
       const int J = R.J[dd], hB = R.hB[dd];
       double *prev = ph->lev[warp][0], *next = ph->lev[warp][1];
@@ -978,24 +981,31 @@ __device__ __forceinline__ double kak_step(double x, TC tc, BC bc, const double 
 }
 
 // Branch-free form for the latency-bound snapshot walks (a warp holds
-// orbits of different bases, so the branchy form diverges every step):
-// the bracket is the number of cached thresholds >= 1 - x (they decrease),
-// the increment is picked by a select tree on its bits.
+// orbits of different bases, so the branchy form diverges every step).  The
+// thresholds decrease, so c_j = (1 - x <= thr_j) holds exactly for j < k;
+// all eight candidates x + b_j are formed next to 1 - x and the result is
+// picked by a depth-3 select tree on the c_j -- the dependent chain per step
+// is one DADD, one compare and three selects.
 __device__ __forceinline__ double kak_step_flat(double x, const double *tc, const double *bc,
                                                 const double *thr, const double *b) {
   const double om = 1.0 - x;
-  int k = 0;
+  double v[KK_NB];
+  bool c[KK_NB];
 #pragma unroll
-  for (int j = 0; j < KK_NB; j++) k += om <= tc[j] ? 1 : 0;
-  if (k == KK_NB) {  // deeper than the cache: rare
-    while (k < KK_TAB - 1 && om <= thr[k]) k++;
-    const double v = x + b[k];
-    return v >= 1.0 ? v - 1.0 : v;
+  for (int j = 0; j < KK_NB; j++) {
+    v[j] = x + bc[j];
+    c[j] = om <= tc[j];
   }
-  const double s01 = (k & 1) ? bc[1] : bc[0], s23 = (k & 1) ? bc[3] : bc[2];
-  const double s45 = (k & 1) ? bc[5] : bc[4], s67 = (k & 1) ? bc[7] : bc[6];
-  const double s03 = (k & 2) ? s23 : s01, s47 = (k & 2) ? s67 : s45;
-  return x + ((k & 4) ? s47 : s03);
+  if (c[KK_NB - 1]) {  // deeper than the cache: rare
+    int k = KK_NB;
+    while (k < KK_TAB - 1 && om <= thr[k]) k++;
+    const double vv = x + b[k];
+    return vv >= 1.0 ? vv - 1.0 : vv;
+  }
+  const double s01 = c[0] ? v[1] : v[0], s23 = c[2] ? v[3] : v[2];
+  const double s45 = c[4] ? v[5] : v[4], s67 = c[6] ? v[7] : v[6];
+  const double s03 = c[1] ? s23 : s01, s47 = c[5] ? s67 : s45;
+  return c[3] ? s47 : s03;
 }
 
 struct KakDim {  // one base's brackets in registers
