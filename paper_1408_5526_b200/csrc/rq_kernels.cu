@@ -34,6 +34,9 @@
 #ifndef RQ_MBS_MG
 #define RQ_MBS_MG 4  // MBS months evaluated together (ILP across months)
 #endif
+#ifndef RQ_LIBOR_SMEM_RATES
+#define RQ_LIBOR_SMEM_RATES 40  // LIBOR S=80: forward rates kept in shared memory (0: all in registers)
+#endif
 #ifndef RQ_MINB_SMALL
 #define RQ_MINB_SMALL 4  // CTAs per SM targeted for LIBOR S <= 20 (register budget)
 #endif
@@ -195,6 +198,23 @@ struct RasrapDirectShared {
 };
 struct NoShared {
   int unused;
+};
+
+// models with a dynamic shared-memory region (after the tile / generator's)
+template <class M>
+struct ModelDyn {
+  template <class T>
+  static constexpr bool has(decltype(&T::dyn_bytes)) { return true; }
+  template <class T>
+  static constexpr bool has(...) { return false; }
+  static constexpr bool value = has<M>(nullptr);
+  static __host__ __device__ size_t bytes() {
+    if constexpr (value) return M::dyn_bytes();
+    else return 0;
+  }
+  static __device__ __forceinline__ void give(M &m, double *p) {
+    if constexpr (value) m.set_dyn(p);
+  }
 };
 
 // kernels hand the phase-shared buffers to generators that use them
@@ -1241,13 +1261,30 @@ template <int S>
 struct ModelLibor {
   static constexpr bool NORMALS = true;
   static constexpr bool SMALL_LIBOR = S <= 20;
-  static constexpr int MINB = S <= 20 ? RQ_MINB_SMALL : (S <= 40 ? 3 : 2);  // CTAs/SM
+  static constexpr int MINB =
+      S <= 20 ? RQ_MINB_SMALL : (S <= 40 ? 3 : (RQ_LIBOR_SMEM_RATES ? 3 : 2));  // CTAs/SM
   struct Shared {
     double l0[S];
   };
   static __host__ __device__ int gen_dims(int dim) { return dim; }
+  // S = 80: the first NS rates live in dynamic shared memory Ls[NS][TILE]
+  // (they die first: step i only touches rates n >= i), the rest in
+  // registers, so a thread needs ~100 fewer registers and three CTAs fit an
+  // SM instead of two.
+  static constexpr int NS = S >= 80 ? RQ_LIBOR_SMEM_RATES : 0;
+  static __host__ __device__ size_t dyn_bytes() { return sizeof(double) * NS * TILE; }
   const Shared *sh;
-  double L[S];
+  double *Ls;
+  double L[S - NS];
+  __device__ void set_dyn(double *p) { Ls = p; }
+  __device__ __forceinline__ double &Lr(int n) {
+    if (n < NS) return Ls[n * TILE + threadIdx.x];
+    return L[n - NS];
+  }
+  __device__ __forceinline__ double Lv(int n) const {
+    if (n < NS) return Ls[n * TILE + threadIdx.x];
+    return L[n - NS];
+  }
   double delta, s2d, ssq, strike, ff;
   __device__ void init(const ModelParams &mp_, Shared &s) {
     for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.table[n];
@@ -1260,7 +1297,7 @@ struct ModelLibor {
   }
   __device__ void begin() {
 #pragma unroll
-    for (int n = 0; n < S; n++) L[n] = sh->l0[n];
+    for (int n = 0; n < S; n++) Lr(n) = sh->l0[n];
   }
   // static step (S <= CHUNK: whole triangle unrolled, i compile-time)
   __device__ __forceinline__ void step(int i, double z) {
@@ -1269,9 +1306,9 @@ struct ModelLibor {
 #pragma unroll
     for (int n = 0; n < S; n++) {
       if (n >= i) {
-        double r = rcp1(fma(delta, L[n], 1.0));
-        drift = fma(s2d * L[n], r, drift);
-        L[n] *= fma(drift, delta, g1);
+        double r = rcp1(fma(delta, Lr(n), 1.0));
+        drift = fma(s2d * Lr(n), r, drift);
+        Lr(n) *= fma(drift, delta, g1);
       }
     }
   }
@@ -1283,19 +1320,20 @@ struct ModelLibor {
   __device__ __forceinline__ void group(int g, int i, double g1, double &drift, bool partial) {
     double r[GRP];
 #pragma unroll
-    for (int k = 0; k < GRP; k++) r[k] = rcp1(fma(delta, L[g * GRP + k], 1.0));
+    for (int k = 0; k < GRP; k++) r[k] = rcp1(fma(delta, Lr(g * GRP + k), 1.0));
 #pragma unroll
     for (int k = 0; k < GRP; k++) {
       const int n = g * GRP + k;
-      const double dn = fma(s2d * L[n], r[k], drift);
-      const double ln = L[n] * fma(dn, delta, g1);
+      const double ln0 = Lr(n);
+      const double dn = fma(s2d * ln0, r[k], drift);
+      const double ln = ln0 * fma(dn, delta, g1);
       if (partial) {
         const bool alive = n >= i;
         drift = alive ? dn : drift;
-        L[n] = alive ? ln : L[n];
+        Lr(n) = alive ? ln : ln0;
       } else {
         drift = dn;
-        L[n] = ln;
+        Lr(n) = ln;
       }
     }
   }
@@ -1321,8 +1359,8 @@ struct ModelLibor {
   __device__ double payoff() const {
     double prod = 1.0;
 #pragma unroll
-    for (int n = 0; n < S - 1; n++) prod *= fma(delta, L[n], 1.0);
-    const double lt = L[S - 1];
+    for (int n = 0; n < S - 1; n++) prod *= fma(delta, Lv(n), 1.0);
+    const double lt = Lv(S - 1);
     const double pay = delta * fmax(lt - strike, 0.0);
     return pay * ff * rcp2(fma(delta, lt, 1.0) * prod);
   }
@@ -1512,6 +1550,7 @@ __global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathAr
   __shared__ typename Mdl::Shared msh;
   Mdl md;
   md.init(a.mp, msh);
+  ModelDyn<Mdl>::give(md, z + CHUNK * TILE);
   const int warp = threadIdx.x >> 5;
   const int gdims = Mdl::gen_dims(a.mp.dim);
   G g;
@@ -1610,6 +1649,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
   g.setup(a.t, gsh, q.scratch + (size_t)blockIdx.x * dim * TILE);
   if constexpr (!G::RUNS || std::is_same<G, GenKakutaniRuns>::value) g.set_seq(q, dim);
   g.set_dyn(z + CHUNK * TILE);
+  ModelDyn<Mdl>::give(md, z + CHUNK * TILE + G::dyn_bytes(dim) / sizeof(double));
   __syncthreads();
   const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
   const int64_t nunits = (int64_t)a.rep_n * q.segs_per_rep;
@@ -1813,6 +1853,7 @@ __global__ void __launch_bounds__(TILE) k_payoffs_u(ModelParams mp, const double
   extern __shared__ __align__(16) double zt[];  // ZT_BYTES
   Mdl md;
   md.init(mp, msh);
+  ModelDyn<Mdl>::give(md, zt + CHUNK * TILE);
   __syncthreads();
   int64_t p = (int64_t)blockIdx.x * TILE + threadIdx.x;
   const bool ok = p < npaths;
@@ -1993,7 +2034,7 @@ template <class G, class Mdl>
 static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                             int *blocks_out) {
   const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
-  size_t dyn = prep_dyn(k_paths<G, Mdl>, ZT_BYTES);
+  size_t dyn = prep_dyn(k_paths<G, Mdl>, ZT_BYTES + ModelDyn<Mdl>::bytes());
   int blocks = persistent_blocks(k_paths<G, Mdl>, work, dyn);
   if (blocks_out) *blocks_out = blocks;
   if (probe) return cudaSuccess;
@@ -2095,7 +2136,8 @@ cudaError_t launch_mt_snap(const RepTables &t, int rep_local0, int rep_n, const 
 template <class G, class Mdl>
 static cudaError_t seq_gm(const PathArgs &a, const SeqArgs &q, int blocks, int *launched,
                           cudaStream_t s, int *occ) {
-  size_t dyn = prep_dyn(k_paths_seq<G, Mdl>, ZT_BYTES + G::dyn_bytes(a.mp.dim));
+  size_t dyn =
+      prep_dyn(k_paths_seq<G, Mdl>, ZT_BYTES + G::dyn_bytes(a.mp.dim) + ModelDyn<Mdl>::bytes());
   if (occ) {
     *occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_paths_seq<G, Mdl>, TILE, dyn);
@@ -2204,7 +2246,12 @@ cudaError_t launch_model_payoffs(const ModelParams &mp, const double *u, int64_t
     case 10: k_payoffs_u<ModelLibor<10>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
     case 20: k_payoffs_u<ModelLibor<20>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
     case 40: k_payoffs_u<ModelLibor<40>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
-    case 80: k_payoffs_u<ModelLibor<80>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
+    case 80: {
+      const size_t dyn = prep_dyn(k_payoffs_u<ModelLibor<80>>,
+                                  ZT_BYTES + ModelDyn<ModelLibor<80>>::bytes());
+      k_payoffs_u<ModelLibor<80>><<<blocks, TILE, dyn, s>>>(mp, u, npaths, out);
+      break;
+    }
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
