@@ -890,8 +890,18 @@ int rq_run_replications(int generator, const rq_model *model, uint64_t seed, int
   if (rep_count < 1) return fail(RQ_ERR_VALUE, "need at least one replication");
   int rc = check_grid(grid_host, ngrid);
   if (rc) return rc;
-  static cudaStream_t st = nullptr;
-  if (!st) RQ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  // one non-blocking stream per device (a process may drive several GPUs)
+  static std::mutex smu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  RQ_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(RQ_ERR_VALUE, "device ordinal %d out of range", dev);
+  cudaStream_t st;
+  {
+    std::lock_guard<std::mutex> lk(smu);
+    if (!streams[dev]) RQ_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    st = streams[dev];
+  }
   double *theta_dev = nullptr;
   RQ_CUDA(cudaMallocAsync((void **)&theta_dev, sizeof(double) * rep_count * ngrid, st));
   // replication groups bound the randomisation tables (<= ~256 MiB)
