@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -53,6 +54,14 @@ struct KTimer {  // CUDA events on the launching stream when timing is on
     }
   }
 };
+
+// size knobs, overridable for tests that exercise the batch / group loops
+int64_t env_int(const char *name, int64_t dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  const long long x = std::atoll(v);
+  return x > 0 ? (int64_t)x : dflt;
+}
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -670,7 +679,8 @@ static int seq_begin(const rq::RepTables &t, const rq::ModelParams &mp, int B, i
                                   (rq::kak_runs(t.dim) ? 128 : 1);
   // the walk is latency bound (its time hardly depends on the group size):
   // few, large groups (<= 1 GiB of snapshots)
-  int64_t G = std::max<int64_t>(B, ((int64_t)1024 << 20) / (int64_t)per_rep / B * B);
+  int64_t G = std::max<int64_t>(B, env_int("RQ_SNAP_GROUP_BYTES", (int64_t)1024 << 20) /
+                                      (int64_t)per_rep / B * B);
   G = std::min<int64_t>(G, t.rep_count);
   R.grp_cap = G;
   size_t b_scr = (mt ? sizeof(uint32_t) : sizeof(double)) * (size_t)R.ctas * t.dim * 128;
@@ -831,7 +841,7 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
   if ((rc = model_to_params(model, s->t.dim, mp, &tab, st))) return rc;
   const int64_t nmax = grid_host[ngrid - 1];
   // replication batch: payoff buffer <= 1 GiB (2^27 paths), >= 1 replication
-  int64_t B = std::max<int64_t>(1, ((int64_t)128 << 20) / nmax);
+  int64_t B = std::max<int64_t>(1, env_int("RQ_BATCH_PATHS", (int64_t)128 << 20) / nmax);
   B = std::min<int64_t>(B, s->t.rep_count);
   std::vector<HostPlan> hplans(ngrid);
   std::vector<DevPlan> dplans(ngrid);

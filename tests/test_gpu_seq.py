@@ -219,3 +219,16 @@ def test_kakutani_theta_vs_oracle_large(P, oracle):
     got = estimate_replications("kakutani", lib, SEED, 2, 3, (200_003,))
     ref = oracle.run_replications("kakutani", lib, SEED, 2, 3, (200_003,), threads=3)
     assert (np.abs(got / ref - 1)).max() <= THETA_RTOL
+
+
+@pytest.mark.parametrize("gen", ["twister", "xorwow", "kakutani", "rasrap-recursive"])
+def test_small_batches_and_snapshot_groups(P, gen, monkeypatch):
+    """Many payoff batches and snapshot groups give the same theta as one."""
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    model = _model("s20")
+    ref = estimate_replications(gen, model, SEED, 1, 7, (5000, 20_000))
+    monkeypatch.setenv("RQ_BATCH_PATHS", "40000")      # 2 replications per batch
+    monkeypatch.setenv("RQ_SNAP_GROUP_BYTES", "1")      # one batch per snapshot group
+    got = estimate_replications(gen, model, SEED, 1, 7, (5000, 20_000))
+    assert np.array_equal(got, ref)
