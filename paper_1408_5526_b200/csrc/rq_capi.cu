@@ -785,8 +785,8 @@ static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, doub
   if (!m) return fail(RQ_ERR_VALUE, "model is NULL");
   if (m->kind < 0 || m->kind > rq::MODEL_CONST1) return fail(RQ_ERR_VALUE, "unknown model kind %d", m->kind);
   if (m->dim != dim) return fail(RQ_ERR_VALUE, "model dim %d != sampler dim %d", m->dim, dim);
-  if (m->kind == rq::MODEL_LIBOR && !(m->dim == 10 || m->dim == 20 || m->dim == 40 || m->dim == 80))
-    return fail(RQ_ERR_VALUE, "LIBOR steps %d not compiled (10, 20, 40, 80)", m->dim);
+  if (m->kind == rq::MODEL_LIBOR && (m->dim < 1 || m->dim > rq::LIBOR_DYN_MAX))
+    return fail(RQ_ERR_VALUE, "LIBOR steps %d outside 1..%d", m->dim, rq::LIBOR_DYN_MAX);
   mp.kind = m->kind;
   mp.dim = m->dim;
   mp.delta = m->delta;

@@ -10,6 +10,7 @@ constexpr int MAX_DIM = 512;    // Halton/Rasrap dimensions with universal table
 constexpr int MAX_CAP = 40;     // K + 8 for base 2 (largest digit window)
 constexpr int SOBOL_BITS = 32;  // sobol.py:30
 constexpr int CHUNK_DIMS = 20;  // dimensions per generator chunk in the fused kernels
+constexpr int LIBOR_DYN_MAX = 160;  // LIBOR steps of the generic (shared-memory) model
 constexpr int MBS_EXP_TERMS = 10;  // k0 exp(sigma_xi z) polynomial: z^0 .. z^9
 
 enum Gen : int {

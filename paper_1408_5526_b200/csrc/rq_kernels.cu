@@ -208,8 +208,8 @@ struct ModelDyn {
   template <class T>
   static constexpr bool has(...) { return false; }
   static constexpr bool value = has<M>(nullptr);
-  static __host__ __device__ size_t bytes() {
-    if constexpr (value) return M::dyn_bytes();
+  static __host__ __device__ size_t bytes(int dim) {
+    if constexpr (value) return M::dyn_bytes(dim);
     else return 0;
   }
   static __device__ __forceinline__ void give(M &m, double *p) {
@@ -1272,7 +1272,7 @@ struct ModelLibor {
   // registers, so a thread needs ~100 fewer registers and three CTAs fit an
   // SM instead of two.
   static constexpr int NS = S >= 80 ? RQ_LIBOR_SMEM_RATES : 0;
-  static __host__ __device__ size_t dyn_bytes() { return sizeof(double) * NS * TILE; }
+  static __host__ __device__ size_t dyn_bytes(int) { return sizeof(double) * NS * TILE; }
   const Shared *sh;
   double *Ls;
   double L[S - NS];
@@ -1361,6 +1361,64 @@ struct ModelLibor {
 #pragma unroll
     for (int n = 0; n < S - 1; n++) prod *= fma(delta, Lv(n), 1.0);
     const double lt = Lv(S - 1);
+    const double pay = delta * fmax(lt - strike, 0.0);
+    return pay * ff * rcp2(fma(delta, lt, 1.0) * prod);
+  }
+};
+
+// LIBOR with any number of steps S <= LIBOR_DYN_MAX (LiborConfig allows any
+// integer maturity/accrual, models.py:172-193): the same operations per
+// rate-step as ModelLibor<S> (models.py:271-293), the forward rates in
+// dynamic shared memory Ls[S][TILE] and the rate loop dynamic.  The step
+// counts of the benchmark configurations (10, 20, 40, 80) use the
+// register-resident ModelLibor<S> instead.
+struct ModelLiborDyn {
+  static constexpr bool NORMALS = true;
+  static constexpr bool SMALL_LIBOR = false;
+  static constexpr int MINB = 2;
+  struct Shared {
+    double l0[LIBOR_DYN_MAX];
+  };
+  static __host__ __device__ int gen_dims(int dim) { return dim; }
+  static __host__ __device__ size_t dyn_bytes(int dim) { return sizeof(double) * dim * TILE; }
+  const Shared *sh;
+  double *Ls;
+  int S;
+  double delta, s2d, ssq, strike, ff;
+  __device__ void set_dyn(double *p) { Ls = p; }
+  __device__ void init(const ModelParams &mp_, Shared &s) {
+    S = mp_.dim;
+    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.table[n];
+    sh = &s;
+    strike = mp_.strike;
+    ff = mp_.front_factor;
+    delta = mp_.delta;
+    s2d = mp_.sigma * mp_.sigma * mp_.delta;
+    ssq = mp_.sigma * sqrt(mp_.delta);
+  }
+  __device__ void begin() {
+    for (int n = 0; n < S; n++) Ls[n * TILE + threadIdx.x] = sh->l0[n];
+  }
+  __device__ void chunk(int d0, int Dc, const double *zcol) {
+    for (int k = 0; k < Dc; k++) {
+      const int i = d0 + k;
+      const double g1 = fma(ssq, zcol[k * TILE], 1.0);
+      double drift = 0.0;
+      double *L = Ls + threadIdx.x;
+#pragma unroll 4
+      for (int n = i; n < S; n++) {
+        const double ln = L[n * TILE];
+        const double r = rcp1(fma(delta, ln, 1.0));
+        drift = fma(s2d * ln, r, drift);
+        L[n * TILE] = ln * fma(drift, delta, g1);
+      }
+    }
+  }
+  __device__ double payoff() const {
+    const double *L = Ls + threadIdx.x;
+    double prod = 1.0;
+    for (int n = 0; n < S - 1; n++) prod *= fma(delta, L[n * TILE], 1.0);
+    const double lt = L[(S - 1) * TILE];
     const double pay = delta * fmax(lt - strike, 0.0);
     return pay * ff * rcp2(fma(delta, lt, 1.0) * prod);
   }
@@ -2034,7 +2092,7 @@ template <class G, class Mdl>
 static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                             int *blocks_out) {
   const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
-  size_t dyn = prep_dyn(k_paths<G, Mdl>, ZT_BYTES + ModelDyn<Mdl>::bytes());
+  size_t dyn = prep_dyn(k_paths<G, Mdl>, ZT_BYTES + ModelDyn<Mdl>::bytes(a.mp.dim));
   int blocks = persistent_blocks(k_paths<G, Mdl>, work, dyn);
   if (blocks_out) *blocks_out = blocks;
   if (probe) return cudaSuccess;
@@ -2054,6 +2112,8 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
         case 40: return paths_gm<G, ModelLibor<40>>(a, launched, s, probe, blocks);
         case 80: return paths_gm<G, ModelLibor<80>>(a, launched, s, probe, blocks);
       }
+      if (a.mp.dim >= 1 && a.mp.dim <= LIBOR_DYN_MAX)
+        return paths_gm<G, ModelLiborDyn>(a, launched, s, probe, blocks);
       return cudaErrorInvalidValue;
     case MODEL_MBS:
       if (a.mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
@@ -2137,7 +2197,8 @@ template <class G, class Mdl>
 static cudaError_t seq_gm(const PathArgs &a, const SeqArgs &q, int blocks, int *launched,
                           cudaStream_t s, int *occ) {
   size_t dyn =
-      prep_dyn(k_paths_seq<G, Mdl>, ZT_BYTES + G::dyn_bytes(a.mp.dim) + ModelDyn<Mdl>::bytes());
+      prep_dyn(k_paths_seq<G, Mdl>,
+               ZT_BYTES + G::dyn_bytes(a.mp.dim) + ModelDyn<Mdl>::bytes(a.mp.dim));
   if (occ) {
     *occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_paths_seq<G, Mdl>, TILE, dyn);
@@ -2159,6 +2220,8 @@ static cudaError_t seq_g(const PathArgs &a, const SeqArgs &q, int blocks, int *l
         case 40: return seq_gm<G, ModelLibor<40>>(a, q, blocks, launched, s, occ);
         case 80: return seq_gm<G, ModelLibor<80>>(a, q, blocks, launched, s, occ);
       }
+      if (a.mp.dim >= 1 && a.mp.dim <= LIBOR_DYN_MAX)
+        return seq_gm<G, ModelLiborDyn>(a, q, blocks, launched, s, occ);
       return cudaErrorInvalidValue;
     case MODEL_MBS:
       if (a.mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
@@ -2248,11 +2311,16 @@ cudaError_t launch_model_payoffs(const ModelParams &mp, const double *u, int64_t
     case 40: k_payoffs_u<ModelLibor<40>><<<blocks, TILE, ZT_BYTES, s>>>(mp, u, npaths, out); break;
     case 80: {
       const size_t dyn = prep_dyn(k_payoffs_u<ModelLibor<80>>,
-                                  ZT_BYTES + ModelDyn<ModelLibor<80>>::bytes());
+                                  ZT_BYTES + ModelDyn<ModelLibor<80>>::bytes(80));
       k_payoffs_u<ModelLibor<80>><<<blocks, TILE, dyn, s>>>(mp, u, npaths, out);
       break;
     }
-    default: return cudaErrorInvalidValue;
+    default: {
+      if (mp.dim < 1 || mp.dim > LIBOR_DYN_MAX) return cudaErrorInvalidValue;
+      const size_t dyn =
+          prep_dyn(k_payoffs_u<ModelLiborDyn>, ZT_BYTES + ModelDyn<ModelLiborDyn>::bytes(mp.dim));
+      k_payoffs_u<ModelLiborDyn><<<blocks, TILE, dyn, s>>>(mp, u, npaths, out);
+    }
   }
   return cudaGetLastError();
 }

@@ -381,6 +381,30 @@ def test_libor_steps_vs_oracle(P, oracle, mat, acc):
         assert (np.abs(got / ref - 1)).max() <= THETA_RTOL
 
 
+@pytest.mark.parametrize("mat,acc", [(0.25, 0.25), (3.0, 0.25), (7.5, 0.25), (15.0, 0.5),
+                                     (20.0, 0.125)])
+def test_libor_any_steps_vs_oracle(P, oracle, mat, acc):
+    """Step counts without a register kernel (S = 1, 12, 30, 30, 160): the
+    shared-memory LIBOR model, fused paths and model.payoffs(u)."""
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    model = M.LiborModel(M.LiborConfig(maturity=mat, accrual=acc))
+    for gen in ("rasrap-recursive", "philox", "xorwow", "kakutani"):
+        got = estimate_replications(gen, model, SEED, 3, 2, (2000,))
+        ref = _oracle_theta(oracle, gen, model, SEED, 3, 2, (2000,))
+        # (S = 1: the caplet is out of the money on every path, theta == 0)
+        assert (np.abs(got - ref) <= THETA_RTOL * np.abs(ref)).all(), gen
+    u = np.random.default_rng(5).random((700, model.dim))
+    mid, dim, par = oracle.model_params(model)
+    ref = oracle.libor_payoffs(u, par[4:], par[0], par[1], par[2], par[3])
+    got = model.payoffs(u)
+    # per path the caplet's (L - K)^+ cancels near the money (an ulp of L is
+    # ~1e-12 of a small payoff); theta above holds the 1e-12 bar
+    scale = np.maximum(np.abs(ref), np.abs(ref).max() * 1e-3)
+    assert (np.abs(got - ref) <= 10 * PAYOFF_RTOL * scale).all()
+
+
 @pytest.mark.parametrize("cfg", [dict(months=24), dict(months=360, variance=0.0),
                                  dict(months=100, variance=0.0009, initial_rate=0.01)])
 def test_mbs_variants_vs_oracle(P, oracle, cfg):

@@ -111,7 +111,8 @@ def test_libor_config_validation():
     with pytest.raises(ValueError):
         M.LiborConfig(maturity=5.0, accrual=0.3)
     with pytest.raises(ValueError):
-        M.LiborModel(M.LiborConfig(maturity=7.5, accrual=0.25))  # S=30 not compiled
+        M.LiborModel(M.LiborConfig(maturity=50.0, accrual=0.25))  # S=200 > 160
+    assert M.LiborModel(M.LiborConfig(maturity=7.5, accrual=0.25)).dim == 30  # generic model
 
 
 # ------------------------------------------------------------ aggregation
