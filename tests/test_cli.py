@@ -75,3 +75,24 @@ def test_libor_experiment_writes_report(tmp_path):
     assert lines[0] == "generator,model,N,M,mean,std,time_s,efficiency"
     assert len(lines) == 1 + 2 * 3
     assert (tmp_path / "r_summary.csv").exists()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gen", ["rasrap-recursive", "philox", "sobol-gray", "twister",
+                                 "kakutani"])
+def test_bench_throughput_runs(gen):
+    """harness.bench_throughput (harness.py:401-429): raw generation rate."""
+    from paper_1408_5526_b200 import harness
+
+    rate = harness.bench_throughput(gen, 20, 2_000_000, runs=3)
+    assert rate > 1e8  # coordinates/s (the reference's CPU rate is ~1e8 at best)
+
+
+@pytest.mark.gpu
+def test_cli_bench_prints_rate(capsys):
+    from paper_1408_5526_b200 import cli
+
+    assert cli.main(["bench", "--generator", "xorwow", "--dim", "8", "--count", "100000",
+                     "--runs", "2"]) == 0
+    out = capsys.readouterr().out
+    assert out.startswith("xorwow\tdim=8\t") and out.strip().endswith("numbers/s")
