@@ -634,10 +634,20 @@ struct GenSobolDirect {
   }
 };
 
+// u = w 2^-32 exactly: 1 + u is assembled from the bits of w and 1 is
+// subtracted (no int->double conversion on the XU pipe).
+__device__ __forceinline__ double sobol_u(uint32_t w) {
+  return __hiloint2double((int)(0x3FF00000u | (w >> 12)), (int)(w << 20)) - 1.0;
+}
+
 // Tiled Sobol': in a 128-aligned tile the index bits >= 7 are common, so
-// the warp owning a dim folds them and the shift into one word; each point
-// then XORs at most 7 more direction words.  Unaligned tiles (sampler.fill
-// from an odd start) use the per-point loop.
+// the warp owning a dim folds them and the shift into one word.  Lane l
+// takes the points t = l + 32m (m < 4, conflict-free tile rows).  For t < 32
+// the counter index t + 32m differs from t in bits 5-6 only, and the Gray
+// index g(t + 32m) = g(t) ^ (32m ^ 16m) (48, 96, 80: bits 4-6), so each lane
+// forms its word for t from seven direction words and the other three
+// points by one XOR with a warp-uniform word.  Unaligned tiles
+// (sampler.fill from an odd start) use the per-point loop.
 template <bool GRAY>
 struct GenSobolTile {
   const RepTables *t;
@@ -649,27 +659,28 @@ struct GenSobolTile {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool aligned = (base & 127u) == 0u;
     const uint64_t bidx = GRAY ? (base ^ (base >> 1)) : base;
+    const uint32_t gl = GRAY ? (uint32_t)(lane ^ (lane >> 1)) : (uint32_t)lane;
     for (int dd = warp; dd < Dc; dd += WARPS) {
       const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
       if (aligned) {
-        uint32_t hi = sobol_word<false>(vd, shp[d0 + dd], (bidx >> 7) << 7);
-        uint32_t vk[7];
+        // For an aligned base B the (Gray) index of B + t is bidx ^ g(t)
+        // (the bits of B and t, and of B>>1 and t>>1, are disjoint), so the
+        // lane's low 7 bits are c = (bidx & 127) ^ g(lane)
+        uint32_t x = sobol_word<false>(vd, shp[d0 + dd], (bidx >> 7) << 7);
+        const uint32_t c = ((uint32_t)bidx & 127u) ^ gl;
 #pragma unroll
-        for (int k = 0; k < 7; k++) vk[k] = vd[k];
-#pragma unroll 2
-        for (int m = 0; m < TILE / 32; m++) {
-          const uint32_t tt = (uint32_t)(lane + 32 * m);
-          const uint32_t i = (uint32_t)base + tt;
-          const uint32_t g = (GRAY ? (i ^ (i >> 1)) : i) & 127u;
-          uint32_t x = hi;
-#pragma unroll
-          for (int k = 0; k < 7; k++) x ^= (g >> k) & 1u ? vk[k] : 0u;
-          zt[dd * TILE + tt] = (double)x * TWO_M32;
-        }
+        for (int k = 0; k < 7; k++) x ^= (c >> k) & 1u ? __ldg(vd + k) : 0u;
+        const uint32_t v4 = __ldg(vd + 4), v5 = __ldg(vd + 5), v6 = __ldg(vd + 6);
+        const uint32_t w1 = GRAY ? v4 ^ v5 : v5, w2 = GRAY ? v5 ^ v6 : v6;
+        const uint32_t w3 = GRAY ? v4 ^ v6 : v5 ^ v6;
+        double *row = zt + dd * TILE + lane;
+        row[0] = sobol_u(x);
+        row[32] = sobol_u(x ^ w1);
+        row[64] = sobol_u(x ^ w2);
+        row[96] = sobol_u(x ^ w3);
       } else {
         for (int tt = lane; tt < TILE; tt += 32)
-          zt[dd * TILE + tt] =
-              (double)sobol_word<GRAY>(vd, shp[d0 + dd], base + (uint64_t)tt) * TWO_M32;
+          zt[dd * TILE + tt] = sobol_u(sobol_word<GRAY>(vd, shp[d0 + dd], base + (uint64_t)tt));
       }
     }
   }
