@@ -53,6 +53,7 @@ constexpr double TWO_M53 = 1.1102230246251565e-16;  // 2^-53
 __constant__ HaltonDim c_hdim[MAX_DIM];
 constexpr int CWTS = 1280;  // binpow weights of the first dims, in the constant bank
 static_assert(CHUNK_DIMS <= 40, "persistent Rasrap tiles assume their weights fit c_wts");
+static_assert(CHUNK_DIMS <= 20, "persistent Rasrap tiles stage sigma of <= 20 dims (639 entries)");
 __constant__ double c_wts[CWTS];
 constexpr int WTS_CAP = 16384;
 __device__ double g_wts[WTS_CAP];     // binpow(inv_p, j+1): numba `x ** int` (halton.py:409)
@@ -299,13 +300,16 @@ struct GenRasrapRecTile {
   const RepTables *t;
   Shared *sh;
   PhaseShared *ph;  // level buffers (aliased with the tail queues, see PhaseShared)
-  bool persist;   // consecutive tiles of one CTA share a persistent stream state
-  bool sig_smem;  // sigma of the dims staged in shared memory as doubles
-  __device__ void setup(const RepTables &t_, Shared &s, int gdims = 0) {
+  // PERSIST (dispatch: single-chunk models, <= CHUNK dims): consecutive tiles
+  // of one CTA share a persistent stream state and the dims' sigma tables are
+  // staged in shared memory as doubles (the first CHUNK primes sum to 639 <=
+  // SIGD_MAX).  Compile-time, so the persistent kernel carries no stateless
+  // or global-sigma code (instruction-cache footprint).
+  static constexpr bool persist = PERSIST;
+  static constexpr bool sig_smem = PERSIST;
+  __device__ void setup(const RepTables &t_, Shared &s, int = 0) {
     t = &t_;
     sh = &s;
-    persist = PERSIST && gdims > 0 && gdims <= CHUNK;
-    sig_smem = persist && c_hdim[gdims - 1].sig_off + c_hdim[gdims - 1].base <= SIGD_MAX;
     for (int k = threadIdx.x; k < CHUNK; k += TILE) s.st_rl[k] = -1;
   }
   // Full state at B = n0 + base: digits, hB, P[j] = S_j(B) (chain from
