@@ -60,11 +60,17 @@ NORMAL_SLOTS = 36  # Phi^-1 per normal
 TRAFFIC_SOURCE = "profiles/traffic.json (ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum)"
 
 
-def traffic_per_launch(workload: str, gen: str, M: int, N: int):
+def _profile_entry(workload: str, gen: str) -> dict:
     try:
         tab = json.loads((ROOT / "profiles" / "traffic.json").read_text())
-        bpp = tab[f"{workload}/{gen}"]["dram_bytes_per_path"]
+        return tab[f"{workload}/{gen}"]
     except (OSError, KeyError, ValueError):
+        return {}
+
+
+def traffic_per_launch(workload: str, gen: str, M: int, N: int):
+    bpp = _profile_entry(workload, gen).get("dram_bytes_per_path")
+    if bpp is None:
         return None
     per_launch = min(M, max(1, (128 << 20) // N)) * N  # rq_estimate's replication batch
     return bpp * per_launch
@@ -340,6 +346,7 @@ def run_ours(args) -> dict:
                               "reduce": ks["reduce_ms"]},
                 "traffic": traffic_per_launch(args.workload, gen, M, N),
                 "traffic_source": TRAFFIC_SOURCE,
+                "ncu_fp64_pipe_pct": _profile_entry(args.workload, gen).get("fp64_pipe_pct"),
             },
             "e2e": {"value": e2e_value, "unit": "paths/s",
                     "h2d_bytes_per_step": tr["h2d"] // ne, "d2h_bytes_per_step": tr["d2h"] // ne,

@@ -37,6 +37,9 @@
 #ifndef RQ_LIBOR_SMEM_RATES
 #define RQ_LIBOR_SMEM_RATES 40  // LIBOR S=80: forward rates kept in shared memory (0: all in registers)
 #endif
+#ifndef RQ_LIBOR_STATIC_MAX
+#define RQ_LIBOR_STATIC_MAX 20  // LIBOR steps up to which the rate triangle is fully unrolled
+#endif
 #ifndef RQ_MINB_SMALL
 #define RQ_MINB_SMALL 4  // CTAs per SM targeted for LIBOR S <= 20 (register budget)
 #endif
@@ -1364,7 +1367,7 @@ struct ModelLibor {
     }
   }
   __device__ void chunk(int d0, int Dc, const double *zcol) {
-    if (S <= CHUNK) {
+    if (S <= CHUNK && S <= RQ_LIBOR_STATIC_MAX) {
 #pragma unroll
       for (int i = 0; i < S; i++) step(i, zcol[i * TILE]);
     } else {
