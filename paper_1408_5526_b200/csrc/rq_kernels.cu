@@ -26,6 +26,8 @@
 
 #include <cstdint>
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <type_traits>
 
 #include "rq_device.cuh"
@@ -960,7 +962,7 @@ struct GenTwister {
 // (halton.py:226-235); that k is unique (the smallest k with
 // 1 - x > thr[k-1], thr = inv_pow + tol in double), so the device scans the
 // thresholds directly.  Orbits are sequential: segments start from
-// snapshots taken by k_kak_snap.
+// snapshots taken by k_kak_walk.
 // ======================================================================
 __device__ double g_kk_thr[MAX_DIM * KK_TAB];
 __device__ double g_kk_b[MAX_DIM * KK_TAB];
@@ -969,7 +971,23 @@ __device__ double g_kk_b[MAX_DIM * KK_TAB];
 // warp-uniform reads from the constant bank
 __constant__ double c_kk8[KK_RUNS_MAXDIM * 16];
 
+__device__ double g_kk_xthr[MAX_DIM * 8];  // see kak_step_flat
+
+static double kak_xthr(double thr) {  // smallest double x with fl(1 - x) <= thr
+  double x = 1.0 - thr;
+  while (!(1.0 - x <= thr)) x = std::nextafter(x, 2.0);
+  while (x > 0.0 && 1.0 - std::nextafter(x, -1.0) <= thr) x = std::nextafter(x, -1.0);
+  return x;
+}
+
 cudaError_t upload_kakutani_tables(const double *thr, const double *b, int dims) {
+  {
+    std::vector<double> xt((size_t)dims * 8);
+    for (int d = 0; d < dims; d++)
+      for (int j = 0; j < 8; j++) xt[(size_t)d * 8 + j] = kak_xthr(thr[d * KK_TAB + j]);
+    cudaError_t e0 = cudaMemcpyToSymbol(g_kk_xthr, xt.data(), sizeof(double) * xt.size());
+    if (e0 != cudaSuccess) return e0;
+  }
   cudaError_t e = cudaMemcpyToSymbol(g_kk_thr, thr, sizeof(double) * dims * KK_TAB);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyToSymbol(g_kk_b, b, sizeof(double) * dims * KK_TAB);
@@ -1019,31 +1037,28 @@ __device__ __forceinline__ double kak_step(double x, TC tc, BC bc, const double 
 }
 
 // Branch-free form for the latency-bound snapshot walks (a warp holds
-// orbits of different bases, so the branchy form diverges every step).  The
-// thresholds decrease, so c_j = (1 - x <= thr_j) holds exactly for j < k;
-// all eight candidates x + b_j are formed next to 1 - x and the result is
-// picked by a depth-3 select tree on the c_j -- the dependent chain per step
-// is one DADD, one compare and three selects.
-__device__ __forceinline__ double kak_step_flat(double x, const double *tc, const double *bc,
+// orbits of different bases, so the branchy form diverges every step).  As
+// fl(1 - x) does not increase with x, the bracket test 1 - x <= thr_j is
+// exactly x >= xthr_j (g_kk_xthr, the smallest such double); the tests hold
+// exactly for j < k, the increment b_k is picked by a depth-3 select tree
+// and added once: the dependent chain per step is a compare, three selects
+// and one DADD.
+__device__ __forceinline__ double kak_step_flat(double x, const double *xc, const double *bc,
                                                 const double *thr, const double *b) {
-  const double om = 1.0 - x;
-  double v[KK_NB];
   bool c[KK_NB];
 #pragma unroll
-  for (int j = 0; j < KK_NB; j++) {
-    v[j] = x + bc[j];
-    c[j] = om <= tc[j];
-  }
+  for (int j = 0; j < KK_NB; j++) c[j] = x >= xc[j];
   if (c[KK_NB - 1]) {  // deeper than the cache: rare
+    const double om = 1.0 - x;
     int k = KK_NB;
     while (k < KK_TAB - 1 && om <= thr[k]) k++;
     const double vv = x + b[k];
     return vv >= 1.0 ? vv - 1.0 : vv;
   }
-  const double s01 = c[0] ? v[1] : v[0], s23 = c[2] ? v[3] : v[2];
-  const double s45 = c[4] ? v[5] : v[4], s67 = c[6] ? v[7] : v[6];
+  const double s01 = c[0] ? bc[1] : bc[0], s23 = c[2] ? bc[3] : bc[2];
+  const double s45 = c[4] ? bc[5] : bc[4], s67 = c[6] ? bc[7] : bc[6];
   const double s03 = c[1] ? s23 : s01, s47 = c[5] ? s67 : s45;
-  return c[3] ? s47 : s03;
+  return x + (c[3] ? s47 : s03);
 }
 
 struct KakDim {  // one base's brackets in registers
@@ -1062,9 +1077,6 @@ struct KakDim {  // one base's brackets in registers
     return kak_step(
         x, [&](int j) { return tc[j]; }, [&](int j) { return bc[j]; }, thr, b);
   }
-  __device__ __forceinline__ double step_flat(double x) const {
-    return kak_step_flat(x, tc, bc, thr, b);
-  }
 };
 
 // x0 of every (replication, dim): KakutaniState(p, rng.random()) with
@@ -1079,45 +1091,55 @@ __global__ void k_kakutani_setup(RepTables t, double *x0) {
   x0[gid] = pcg_random(g);
 }
 
-// Orbit points at the segment starts P_s = p0 + s seg_len, one thread per
-// (replication of the group, dim); point n is x after n steps.
-__global__ void k_kak_snap(RepTables t, int rep_local0, int rep_n, SeqArgs q, double *snap) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)rep_n * t.dim) return;
-  const int rb = (int)(gid / t.dim), d = (int)(gid % t.dim);
-  KakDim kd;
-  kd.load(d);
-  double x = t.kk_x0[(int64_t)(rep_local0 + rb) * t.dim + d];
-  int64_t pos = 0;
-  for (int sg = 0; sg < q.segs_per_rep; sg++) {
-    const int64_t P = q.p0 + (int64_t)sg * q.seg_len;
-#pragma unroll 4
-    for (; pos < P; pos++) x = kd.step_flat(x);
-    snap[((int64_t)rb * q.segs_per_rep + sg) * t.dim + d] = x;
-  }
-}
 
-// Orbit points at the run starts of every segment (the per-thread runs
-// layout): P = p0 + s seg_len + t ntile_s, t < TILE.
-__global__ void k_kak_snap_runs(RepTables t, int rep_local0, int rep_n, SeqArgs q,
-                                double *snap) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)rep_n * t.dim) return;
-  const int rb = (int)(gid / t.dim), d = (int)(gid % t.dim);
-  KakDim kd;
-  kd.load(d);
-  double x = t.kk_x0[(int64_t)(rep_local0 + rb) * t.dim + d];
+// Snapshot walk: orbit points at the segment starts P_s = p0 + s seg_len
+// (tile layout) or at every run start P = p0 + s seg_len + t ntile_s, t <
+// TILE (runs layout); point n is x after n steps.  Each orbit is one
+// dependent chain of up to N steps (latency bound), so a thread walks
+// KAK_KW orbits interleaved.
+constexpr int KAK_KW = 1;  // orbits per thread (4 measured slower: fewer warps, same chain)
+template <bool RUNS_LAYOUT>
+__global__ void k_kak_walk(RepTables t, int rep_local0, int rep_n, SeqArgs q, double *snap) {
+  const int64_t norb = (int64_t)rep_n * t.dim;
+  const int64_t o0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * KAK_KW;
+  if (o0 >= norb) return;
+  double xc[KAK_KW][KK_NB], bc[KAK_KW][KK_NB], x[KAK_KW];
+  const double *thr[KAK_KW], *bb[KAK_KW];
+  int64_t base[KAK_KW];  // snapshot offset of the orbit
+  bool ok[KAK_KW];
+#pragma unroll
+  for (int w = 0; w < KAK_KW; w++) {
+    ok[w] = o0 + w < norb;
+    const int64_t o = ok[w] ? o0 + w : o0;
+    const int rb = (int)(o / t.dim), d = (int)(o % t.dim);
+    thr[w] = g_kk_thr + d * KK_TAB;
+    bb[w] = g_kk_b + d * KK_TAB;
+#pragma unroll
+    for (int j = 0; j < KK_NB; j++) {
+      xc[w][j] = g_kk_xthr[d * 8 + j];
+      bc[w][j] = bb[w][j];
+    }
+    x[w] = t.kk_x0[(int64_t)(rep_local0 + rb) * t.dim + d];
+    base[w] = (int64_t)rb * q.segs_per_rep * (RUNS_LAYOUT ? TILE : 1) * t.dim + d;
+  }
   int64_t pos = 0;
+  const int nrun = RUNS_LAYOUT ? TILE : 1;
   for (int sg = 0; sg < q.segs_per_rep; sg++) {
     const int64_t s0 = (int64_t)sg * q.seg_len;
     const int64_t slen = q.seg_len < q.nmax - s0 ? q.seg_len : q.nmax - s0;
     const int64_t ntile = (slen + TILE - 1) / TILE;
-    for (int tt = 0; tt < TILE; tt++) {
+    for (int tt = 0; tt < nrun; tt++) {
       int64_t P = q.p0 + s0 + (int64_t)tt * ntile;
       if (P > q.p0 + s0 + slen) P = q.p0 + s0 + slen;  // empty run: never read
-#pragma unroll 4
-      for (; pos < P; pos++) x = kd.step_flat(x);
-      snap[(((int64_t)rb * q.segs_per_rep + sg) * TILE + tt) * t.dim + d] = x;
+#pragma unroll 2
+      for (; pos < P; pos++) {
+#pragma unroll
+        for (int w = 0; w < KAK_KW; w++) x[w] = kak_step_flat(x[w], xc[w], bc[w], thr[w], bb[w]);
+      }
+      const int64_t slot = ((int64_t)sg * nrun + tt) * t.dim;
+#pragma unroll
+      for (int w = 0; w < KAK_KW; w++)
+        if (ok[w]) snap[base[w] + slot] = x[w];
     }
   }
 }
@@ -2198,10 +2220,11 @@ cudaError_t launch_kak_snap(const RepTables &t, int rep_local0, int rep_n, const
                             double *snap, cudaStream_t s) {
   const int64_t n = (int64_t)rep_n * t.dim;
   // latency-bound sequential walks: small CTAs spread them over all SMs
+  const int64_t nthr = (n + KAK_KW - 1) / KAK_KW;
   if (kak_runs(t.dim))
-    k_kak_snap_runs<<<(int)((n + 31) / 32), 32, 0, s>>>(t, rep_local0, rep_n, q, snap);
+    k_kak_walk<true><<<(int)((nthr + 31) / 32), 32, 0, s>>>(t, rep_local0, rep_n, q, snap);
   else
-    k_kak_snap<<<(int)((n + 31) / 32), 32, 0, s>>>(t, rep_local0, rep_n, q, snap);
+    k_kak_walk<false><<<(int)((nthr + 31) / 32), 32, 0, s>>>(t, rep_local0, rep_n, q, snap);
   return cudaGetLastError();
 }
 
