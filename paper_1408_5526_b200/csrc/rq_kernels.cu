@@ -580,6 +580,95 @@ struct GenRasrapCounter {
   }
 };
 
+// Counter form on a tile of TILE consecutive indices n = B + t.  With L the
+// number of base-p digits that cover the tile (p^L > TILE), n = H * p^L + r
+// where r = (B mod p^L) + t and H = B div p^L + (r >= p^L): only two
+// values of H occur in a tile.  The reference's sum runs from the lowest
+// digit up, x = (((s(a0) w0 + s(a1) w1) + ...) (halton.py:431-440), so a
+// point's low L digits are summed per thread and the high terms
+// T_j = s(a_j) w_j of its H (the same products, rounded the same way) are
+// formed once per tile and dim and then added in order: bit-identical, with
+// L instead of max(K, #digits) digit extractions per point.
+constexpr int CT_MAXT = 36;  // high terms per variant (K - L + overflow digits <= 32)
+struct GenRasrapCounterTile {
+  static constexpr int MAXB = 4;
+  struct Shared {
+    double T[CHUNK][2][CT_MAXT];
+    int32_t nT[CHUNK][2];
+    uint32_t lowB[CHUNK];
+  };
+  const RepTables *t;
+  Shared *sh;
+  __device__ void setup(const RepTables &t_, Shared &s, int = 0) {
+    t = &t_;
+    sh = &s;
+  }
+  __device__ void prepare(int rl, uint64_t base, int d, int dd) {  // one lane per dim
+    const HaltonDim &h = c_hdim[d];
+    const uint64_t p = (uint64_t)h.base;
+    const int L = h.tdig + 1;
+    uint64_t pL = 1;
+    for (int j = 0; j < L; j++) pL *= p;
+    const uint64_t B = t->start[(int64_t)rl * t->dim + d] + base;
+    const uint64_t H0 = B / pL;
+    sh->lowB[dd] = (uint32_t)(B - H0 * pL);
+    const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
+    const double *cs = g_cscale + h.sum_off;
+#pragma unroll 1
+    for (int v = 0; v < 2; v++) {
+      uint64_t H = H0 + (uint64_t)v;
+      int j = L, m = 0;
+#pragma unroll 1
+      for (; j < h.K || H != 0u; j++, m++) {
+        const uint64_t q = div_base64(H, h);
+        sh->T[dd][v][m] = dmul(u16d(sg[(uint32_t)(H - q * p)]), cs[j]);
+        H = q;
+      }
+      sh->nT[dd][v] = m;
+    }
+  }
+  __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();  // the previous unit's readers of T are done
+    {
+      const int dd = warp + lane * WARPS;  // 5 dims per warp on lanes 0..4
+      if (dd < Dc) prepare(rl, base, d0 + dd, dd);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int dd = 0; dd < Dc; dd++) {
+      int v;
+      double x = low_sum(rl, d0 + dd, dd, &v);
+      const double *T = sh->T[dd][v];
+      const int n = sh->nT[dd][v];
+#pragma unroll 4
+      for (int m = 0; m < n; m++) x = dadd(x, T[m]);
+      zt[dd * TILE + threadIdx.x] = x;
+    }
+  }
+  // the point's low L digits, summed from the lowest (sets its variant v)
+  __device__ __forceinline__ double low_sum(int rl, int d, int dd, int *v) const {
+    const HaltonDim &h = c_hdim[d];
+    const uint32_t p = (uint32_t)h.base;
+    const int L = h.tdig + 1;
+    uint32_t pL = 1;
+    for (int j = 0; j < L; j++) pL *= p;
+    const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
+    const double *cs = g_cscale + h.sum_off;
+    uint32_t r = sh->lowB[dd] + (uint32_t)threadIdx.x;
+    *v = r >= pL;
+    r = *v ? r - pL : r;
+    double x = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < L; j++) {
+      const uint32_t q = __umulhi(r, h.m16);
+      x = dadd(x, dmul(u16d(sg[r - q * p]), cs[j]));
+      r = q;
+    }
+    return x;
+  }
+};
+
 // u = w 2^-32 + 2^-33 (harness.py:66-67), exactly: the double 1 + u has the
 // mantissa (w << 20) | 2^19, so it is assembled from w with two integer ops
 // and 1 is subtracted exactly (no int->double conversion on the XU pipe).
@@ -2171,7 +2260,7 @@ static cudaError_t paths_dispatch(const PathArgs &a, int *launched, cudaStream_t
       return a.mp.kind == MODEL_MBS || a.mp.dim > CHUNK
                  ? paths_g<GenRasrapRecTile<false>>(a, launched, s, probe, blocks)
                  : paths_g<GenRasrapRecTile<true>>(a, launched, s, probe, blocks);
-    case GEN_RASRAP_COUNTER: return paths_g<GenRasrapCounter>(a, launched, s, probe, blocks);
+    case GEN_RASRAP_COUNTER: return paths_g<GenRasrapCounterTile>(a, launched, s, probe, blocks);
     case GEN_PHILOX: return paths_g<GenPhilox>(a, launched, s, probe, blocks);
     case GEN_SOBOL_GRAY: return paths_g<GenSobolTile<true>>(a, launched, s, probe, blocks);
     case GEN_SOBOL_COUNTER: return paths_g<GenSobolTile<false>>(a, launched, s, probe, blocks);

@@ -443,3 +443,17 @@ def test_many_replications_batched(P, oracle):
     for i in idx:
         ref = _oracle_theta(oracle, "rasrap-recursive", m, SEED, 1 + i, 1, (300_000,))
         assert got[i, 0] == ref[0, 0]
+
+
+def test_rasrap_counter_tiles_bit_exact(P, oracle):
+    """The tiled counter form (low digits per point + shared high terms) at
+    large and ragged N, and through indices above 2^32 - n0: f = x1 theta is
+    bit-exact against the oracle's per-point counter sums."""
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    x1 = M.FirstCoordinateModel()
+    grid = (999_983, 2**20 + 77)
+    got = estimate_replications("rasrap-counter", x1, SEED, 7, 3, grid)
+    ref = oracle.run_replications("rasrap-counter", x1, SEED, 7, 3, grid, threads=3)
+    assert np.array_equal(got, ref)
