@@ -2204,7 +2204,9 @@ cudaError_t launch_points(const RepTables &t, int rl, int64_t first, const int64
     case GEN_RASRAP_RECURSIVE:
       return at ? points_t<GenRasrapRecDirect>(t, rl, first, idx, count, out, s)
                 : points_t<GenRasrapRecTile<false>>(t, rl, first, idx, count, out, s);
-    case GEN_RASRAP_COUNTER: return points_t<GenRasrapCounter>(t, rl, first, idx, count, out, s);
+    case GEN_RASRAP_COUNTER:
+      return at ? points_t<GenRasrapCounter>(t, rl, first, idx, count, out, s)
+                : points_t<GenRasrapCounterTile>(t, rl, first, idx, count, out, s);
     case GEN_PHILOX: return points_t<GenPhilox>(t, rl, first, idx, count, out, s);
     case GEN_SOBOL_GRAY:
       return at ? points_t<GenSobolDirect<true>>(t, rl, first, idx, count, out, s)
@@ -2490,7 +2492,7 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
     case GEN_RASRAP_RECURSIVE:
       return stream_t<GenRasrapRecTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_RASRAP_COUNTER:
-      return stream_t<GenRasrapCounter>(t, rl, npoints, block_sums, nblocks, store, s);
+      return stream_t<GenRasrapCounterTile>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_PHILOX:
       k_stream_reg<GenPhilox><<<nblocks, TILE, 0, s>>>(t, rl, npoints, block_sums, store);
       return cudaGetLastError();

@@ -457,3 +457,17 @@ def test_rasrap_counter_tiles_bit_exact(P, oracle):
     got = estimate_replications("rasrap-counter", x1, SEED, 7, 3, grid)
     ref = oracle.run_replications("rasrap-counter", x1, SEED, 7, 3, grid, threads=3)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("dim", [1, 20, 37, 360])
+def test_rasrap_counter_fill_tiles_vs_oracle(P, oracle, dim):
+    """sampler.fill of the counter form (tiled: shared high terms per tile)
+    from unaligned starts, up to indices near 2^32, == the oracle's counter sums."""
+    from paper_1408_5526_b200.samplers import DeviceSampler
+
+    key = oracle.derive_key(SEED, 4, 3)
+    s = DeviceSampler("rasrap-counter", dim, SEED, 3)
+    for first, count in ((0, 777), (12_345, 1000), (2**32 - 1500, 1500)):
+        got = s.points(first, count).cpu().numpy()
+        ref = oracle.rasrap_counter(dim, key, np.arange(first, first + count, dtype=np.int64))
+        assert np.array_equal(got, ref), (dim, first)
