@@ -308,8 +308,39 @@ __constant__ double c_invn_tnum[8] = {49.41588603624166,  34.09554370467819,  -1
 __constant__ double c_invn_tden[8] = {-0.0005317355830972598, -8.101041244986659, -2.3666362350675305,
                                       19.91298298968798,       -1.4094956335739925, -10.941521790794202,
                                       1.2762506234112334,      1.8704632131064214};
+// ln(pl) for the tail's pl in [2^-53, 0.0465] (normal doubles): pl = m 2^e
+// with m in [sqrt(1/2), sqrt(2)), ln m = 2 atanh(s), s = (m - 1)/(m + 1),
+// |s| <= 0.1716, odd series to s^21 (truncation < 1e-17 absolute), and
+// e ln2 split hi/lo (e * ln2_hi exact).  Absolute error ~1e-16 against
+// |ln pl| >= 3.07: a few ulp, far inside the 2e-13 parity bar, at a third of
+// the instructions of the general libdevice log.
+__constant__ double c_log_ser[10] = {0.047619047619047616, 0.05263157894736842,
+                                     0.058823529411764705, 0.06666666666666667,
+                                     0.07692307692307693,  0.09090909090909091,
+                                     0.1111111111111111,   0.14285714285714285,
+                                     0.2,                  0.3333333333333333};
+__device__ __forceinline__ double log_tail(double pl) {
+  if (pl != pl) return pl;  // NaN in, NaN out (the reference's math.log)
+  int hi = __double2hiint(pl);
+  int e = (hi >> 20) - 1023;
+  hi = (hi & 0x000FFFFF) | 0x3FF00000;  // m in [1, 2)
+  if (hi >= 0x3FF6A09E) {                // m >= ~sqrt(2): use m / 2
+    hi -= 0x00100000;
+    e += 1;
+  }
+  const double m = __hiloint2double(hi, __double2loint(pl));
+  const double f = m - 1.0;  // exact (Sterbenz)
+  const double sv = div2(f, 2.0 + f), s2 = sv * sv;
+  double p = c_log_ser[0];
+#pragma unroll
+  for (int k = 1; k < 10; k++) p = fma(p, s2, c_log_ser[k]);
+  const double t = 2.0 * sv;
+  const double lnm = fma(t * s2, p, t);
+  const double de = (double)e;
+  return fma(de, 0x1.62e42fee00000p-1, fma(de, 1.9082149292705877e-10, lnm));
+}
 __device__ __forceinline__ double invn_tail(double pl) {
-  const double w = (sqrt(-2.0 * log(pl)) - InvNormal::VLO) * InvNormal::VSCALE;
+  const double w = (sqrt(-2.0 * log_tail(pl)) - InvNormal::VLO) * InvNormal::VSCALE;
   double num = c_invn_tnum[0], den = c_invn_tden[0];
 #pragma unroll
   for (int k = 1; k < 8; k++) {

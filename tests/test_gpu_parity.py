@@ -471,3 +471,21 @@ def test_rasrap_counter_fill_tiles_vs_oracle(P, oracle, dim):
         got = s.points(first, count).cpu().numpy()
         ref = oracle.rasrap_counter(dim, key, np.arange(first, first + count, dtype=np.int64))
         assert np.array_equal(got, ref), (dim, first)
+
+
+def test_inv_normal_tail_edges(P, oracle):
+    """The tail's own log (pl = m 2^e, atanh series) over every binade of
+    [2^-53, 0.0465] and at the clamp, against the reference formula."""
+    from paper_1408_5526_b200.models import inv_normal
+
+    e = np.arange(-53, -4)
+    u = np.concatenate([2.0 ** e, np.nextafter(2.0 ** e, 1), 2.0 ** e * 1.4142135,
+                        2.0 ** e * 1.41421357, 2.0 ** e * 1.9999999, [0.0465, 0.04649999999],
+                        1.0 - 2.0 ** e[e > -53], [np.nan, -1.0, 2.0]])
+    u = u[(u < 0.0465) | (u > 0.95) | ~np.isfinite(u) | (u < 0) | (u > 1)]
+    got = inv_normal(u)
+    ref = oracle.inv_normal(u)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    err = np.abs(got[fin] - ref[fin]) / np.maximum(1.0, np.abs(ref[fin]))
+    assert err.max() <= INVN_TOL
