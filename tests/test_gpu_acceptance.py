@@ -86,3 +86,28 @@ def test_criterion_7_paradigm_equivalence():
             rep = P.run_experiment(cfg)
             rows.append([(rep.row(gen, n).mean, rep.row(gen, n).std) for n in (1024, 4096)])
         assert rows[0] == rows[1] == rows[2]
+
+
+@pytest.mark.parametrize("gen", ["sobol-counter", "sobol-gray"])
+def test_criterion_10_dyadic_equidistribution(gen):
+    """test_acceptance.py:270-280 on the device's scrambled points: a linear
+    scramble plus digital shift keeps each coordinate a (0, m, 1)-net, so the
+    first 2^12 points hit every dyadic cell of width 2^-12 once (the Gray
+    order is a permutation of the counter order)."""
+    from paper_1408_5526_b200.samplers import DeviceSampler
+
+    n = 2**12
+    u = DeviceSampler(gen, 360, SEED, 1).points(0, n).cpu().numpy()
+    cells = np.floor(u * n).astype(np.int64)
+    assert all(np.array_equal(np.sort(cells[:, d]), np.arange(n)) for d in range(360))
+
+
+def test_criterion_9_single_month_collapse():
+    """test_acceptance.py:232-237: one month, PV = payment / (1 + i0) for any shock."""
+    from paper_1408_5526_b200 import models as M
+
+    m = M.MbsModel(M.MbsConfig(months=1))
+    u = np.array([[1e-9], [0.5], [0.999], [0.25]])
+    pv = m.payoffs(u)
+    expected = m.config.payment / (1 + m.config.initial_rate)
+    assert np.allclose(pv, expected, rtol=0, atol=1e-15)
