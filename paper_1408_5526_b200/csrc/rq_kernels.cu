@@ -206,6 +206,16 @@ struct NoShared {
   int unused;
 };
 
+// single-chunk models whose chunk width is a compile-time constant
+template <class M>
+struct FixedDims {
+  template <class T>
+  static constexpr int get(decltype(T::FIXED_DIMS) *) { return T::FIXED_DIMS; }
+  template <class T>
+  static constexpr int get(...) { return 0; }
+  static constexpr int value = get<M>(nullptr);
+};
+
 // models with a dynamic shared-memory region (after the tile / generator's)
 template <class M>
 struct ModelDyn {
@@ -1337,10 +1347,13 @@ struct GenKakutani {
 // == order of their bit patterns); four inputs are in flight per pass for
 // ILP; the ~9% tail inputs are queued and evaluated 32 at a time.
 // ======================================================================
-__device__ __forceinline__ void chunk_to_normals(double *zt, int Dc, uint16_t *q) {
+template <int FIXED = 0>  // FIXED > 0: Dc == FIXED known at compile time (no guards)
+__device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *q) {
+  const int Dc = FIXED > 0 ? FIXED : Dc_;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   int qn = 0;
+#pragma unroll
   for (int d4 = 0; d4 < Dc; d4 += 4) {
     double p[4], x[4];
     bool tail[4];
@@ -1390,6 +1403,7 @@ template <int S>
 struct ModelLibor {
   static constexpr bool NORMALS = true;
   static constexpr bool SMALL_LIBOR = S <= 20;
+  static constexpr int FIXED_DIMS = S <= CHUNK ? S : 0;  // one chunk of exactly S dims
   static constexpr int MINB =
       S <= 20 ? RQ_MINB_SMALL : (S <= 40 ? 3 : (RQ_LIBOR_SMEM_RATES ? 3 : 2));  // CTAs/SM
   struct Shared {
@@ -1786,7 +1800,7 @@ __global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathAr
       __syncthreads();
     }
     if (d0 == 0) md.begin();
-    if (Mdl::NORMALS) chunk_to_normals(z, Dc, phs.tq[warp]);
+    if (Mdl::NORMALS) chunk_to_normals<FixedDims<Mdl>::value>(z, Dc, phs.tq[warp]);
     md.chunk(d0, Dc, z + threadIdx.x);
     if (d0 + Dc >= gdims) {
       const int64_t path = base + threadIdx.x;
@@ -1869,7 +1883,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
             for (int dd = 0; dd < Dc; dd++)
               a.payoffs[off * dim + d0 + dd] = z[dd * TILE + threadIdx.x];
         } else {
-          if (Mdl::NORMALS) chunk_to_normals(z, Dc, phs.tq[warp]);
+          if (Mdl::NORMALS) chunk_to_normals<FixedDims<Mdl>::value>(z, Dc, phs.tq[warp]);
           md.chunk(d0, Dc, z + threadIdx.x);
           if (d0 + Dc >= gdims && ok)
             a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + off] = md.payoff();
