@@ -518,7 +518,41 @@ struct GenRasrapRecTile {
       const double *w = g_wts + h.sum_off;
       const int J = R.J[dd], hB = R.hB[dd];
       double *prev = ph->lev[warp][0], *next = ph->lev[warp][1];
-      if (lane == 0) prev[0] = R.sJ[dd];
+      // Levels of <= 32 nodes live in registers, lane k holding node k, and
+      // a child reads its parent with a shuffle (every level above 1 for
+      // p >= 5, and level 1 itself); wider levels go through shared memory.
+      double v = R.sJ[dd];
+      int j = J - 1;
+#pragma unroll 1
+      for (; j >= 1 && R.nn[dd][j] <= 32; j--) {
+        const uint32_t x = (uint32_t)R.bd[dd][j] + (uint32_t)lane;
+        const uint32_t par = __umulhi(x, m16);
+        const uint32_t a = x - par * p;
+        const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
+        const double wj = cw ? c_wts[h.sum_off + j] : w[j];
+        const double vp = __shfl_sync(0xffffffffu, v, (int)par);
+        v = dadd(vp, dmul(sv, wj));
+        if (j > hB && lane == 0) v = ini[j];
+      }
+      if (j == 0) {  // level 0 from the register level 1
+        const uint32_t b0 = R.bd[dd][0];
+        const double w0 = cw ? c_wts[h.sum_off] : w[0];
+        const bool at_n0 = 0 > hB;
+#pragma unroll
+        for (int m = 0; m < TILE / 32; m++) {
+          const int k = lane + 32 * m;
+          const uint32_t x = b0 + (uint32_t)k;
+          const uint32_t par = __umulhi(x, m16);
+          const uint32_t a = x - par * p;
+          const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
+          const double vp = __shfl_sync(0xffffffffu, v, (int)par);
+          double o = dadd(vp, dmul(sv, w0));
+          if (at_n0 && k == 0) o = ini[0];
+          zt[dd * TILE + k] = o;
+        }
+        continue;
+      }
+      prev[lane] = v;  // level j + 1 (<= 32 nodes)
       __syncwarp();
       // one node: S_j(prefix) = S_{j+1}(parent) + sigma(digit) * w_j, or the
       // init sum when the prefix is n0's (node 0 of a level above hB)
@@ -532,7 +566,7 @@ struct GenRasrapRecTile {
         dst[k] = v;
       };
 #pragma unroll 1
-      for (int j = J - 1; j >= 1; j--) {  // upper levels: <= TILE/2 + 2 nodes
+      for (; j >= 1; j--) {  // wide upper levels: <= TILE/2 + 2 nodes
         const int Nj = R.nn[dd][j];
         const uint32_t bj = R.bd[dd][j];
         const double wj = cw ? c_wts[h.sum_off + j] : w[j];
@@ -1391,7 +1425,11 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *
 // ======================================================================
 
 // LIBOR market-model caplet, one-factor Euler (models.py:271-293).  The S
-// forward rates live in registers.  For S <= CHUNK the whole step/rate
+// forward rates live in registers, held as y_n = delta L_n: the reference's
+// rate-step (dl = delta L_n; drift += sigma^2 dl / (1 + dl); L_n *= 1 +
+// drift delta + shock) becomes acc += y_n / (1 + y_n); y_n *= 1 + acc
+// sigma^2 delta + shock, one multiply fewer per rate-step (6 FP64 + MUFU).
+// For S <= CHUNK the whole step/rate
 // triangle is unrolled; above that the step loop is dynamic and the rate
 // loop unrolled with uniform guards.  1/(1 + delta L) in the drift uses a
 // MUFU seed plus one Newton step (the drift's weight in the path is ~1e-4,
@@ -1428,13 +1466,12 @@ struct ModelLibor {
     if (n < NS) return Ls[n * TILE + threadIdx.x];
     return L[n - NS];
   }
-  double delta, s2d, ssq, strike, ff;
+  double s2d, ssq, dstrike, ff;
   __device__ void init(const ModelParams &mp_, Shared &s) {
-    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.table[n];
+    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.delta * mp_.table[n];
     sh = &s;
-    strike = mp_.strike;
+    dstrike = mp_.delta * mp_.strike;
     ff = mp_.front_factor;
-    delta = mp_.delta;
     s2d = mp_.sigma * mp_.sigma * mp_.delta;
     ssq = mp_.sigma * sqrt(mp_.delta);
   }
@@ -1445,13 +1482,13 @@ struct ModelLibor {
   // static step (S <= CHUNK: whole triangle unrolled, i compile-time)
   __device__ __forceinline__ void step(int i, double z) {
     const double g1 = fma(ssq, z, 1.0);
-    double drift = 0.0;
+    double acc = 0.0;
 #pragma unroll
     for (int n = 0; n < S; n++) {
       if (n >= i) {
-        double r = rcp1(fma(delta, Lr(n), 1.0));
-        drift = fma(s2d * Lr(n), r, drift);
-        Lr(n) *= fma(drift, delta, g1);
+        double r = rcp1(1.0 + Lr(n));
+        acc = fma(Lr(n), r, acc);
+        Lr(n) *= fma(acc, s2d, g1);
       }
     }
   }
@@ -1463,13 +1500,13 @@ struct ModelLibor {
   __device__ __forceinline__ void group(int g, int i, double g1, double &drift, bool partial) {
     double r[GRP];
 #pragma unroll
-    for (int k = 0; k < GRP; k++) r[k] = rcp1(fma(delta, Lr(g * GRP + k), 1.0));
+    for (int k = 0; k < GRP; k++) r[k] = rcp1(1.0 + Lr(g * GRP + k));
 #pragma unroll
     for (int k = 0; k < GRP; k++) {
       const int n = g * GRP + k;
       const double ln0 = Lr(n);
-      const double dn = fma(s2d * ln0, r[k], drift);
-      const double ln = ln0 * fma(dn, delta, g1);
+      const double dn = fma(ln0, r[k], drift);
+      const double ln = ln0 * fma(dn, s2d, g1);
       if (partial) {
         const bool alive = n >= i;
         drift = alive ? dn : drift;
@@ -1502,10 +1539,10 @@ struct ModelLibor {
   __device__ double payoff() const {
     double prod = 1.0;
 #pragma unroll
-    for (int n = 0; n < S - 1; n++) prod *= fma(delta, Lv(n), 1.0);
+    for (int n = 0; n < S - 1; n++) prod *= 1.0 + Lv(n);
     const double lt = Lv(S - 1);
-    const double pay = delta * fmax(lt - strike, 0.0);
-    return pay * ff * rcp2(fma(delta, lt, 1.0) * prod);
+    const double pay = fmax(lt - dstrike, 0.0);
+    return pay * ff * rcp2((1.0 + lt) * prod);
   }
 };
 
@@ -1527,15 +1564,14 @@ struct ModelLiborDyn {
   const Shared *sh;
   double *Ls;
   int S;
-  double delta, s2d, ssq, strike, ff;
+  double s2d, ssq, dstrike, ff;
   __device__ void set_dyn(double *p) { Ls = p; }
   __device__ void init(const ModelParams &mp_, Shared &s) {
     S = mp_.dim;
-    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.table[n];
+    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.delta * mp_.table[n];
     sh = &s;
-    strike = mp_.strike;
+    dstrike = mp_.delta * mp_.strike;
     ff = mp_.front_factor;
-    delta = mp_.delta;
     s2d = mp_.sigma * mp_.sigma * mp_.delta;
     ssq = mp_.sigma * sqrt(mp_.delta);
   }
@@ -1546,24 +1582,24 @@ struct ModelLiborDyn {
     for (int k = 0; k < Dc; k++) {
       const int i = d0 + k;
       const double g1 = fma(ssq, zcol[k * TILE], 1.0);
-      double drift = 0.0;
+      double acc = 0.0;
       double *L = Ls + threadIdx.x;
 #pragma unroll 4
       for (int n = i; n < S; n++) {
         const double ln = L[n * TILE];
-        const double r = rcp1(fma(delta, ln, 1.0));
-        drift = fma(s2d * ln, r, drift);
-        L[n * TILE] = ln * fma(drift, delta, g1);
+        const double r = rcp1(1.0 + ln);
+        acc = fma(ln, r, acc);
+        L[n * TILE] = ln * fma(acc, s2d, g1);
       }
     }
   }
   __device__ double payoff() const {
     const double *L = Ls + threadIdx.x;
     double prod = 1.0;
-    for (int n = 0; n < S - 1; n++) prod *= fma(delta, L[n * TILE], 1.0);
+    for (int n = 0; n < S - 1; n++) prod *= 1.0 + L[n * TILE];
     const double lt = L[(S - 1) * TILE];
-    const double pay = delta * fmax(lt - strike, 0.0);
-    return pay * ff * rcp2(fma(delta, lt, 1.0) * prod);
+    const double pay = fmax(lt - dstrike, 0.0);
+    return pay * ff * rcp2((1.0 + lt) * prod);
   }
 };
 
