@@ -1424,11 +1424,22 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *
 // Models: thread-per-path state in registers
 // ======================================================================
 
+// Scale k of the LIBOR rate state z = k delta L: k = sigma^2 delta, the
+// drift's weight, so the drift sum lands directly in the rate multiplier.
+// Below 2^-900 (sigma = 0 included) the drift is below one ulp of the
+// multiplier 1 + shock whatever k is, and k = 2^-900 keeps z normal and
+// 1/k finite.
+__device__ __forceinline__ double libor_state_scale(const ModelParams &mp) {
+  const double s2d = mp.sigma * mp.sigma * mp.delta;
+  return s2d >= 0x1p-900 ? s2d : 0x1p-900;
+}
+
 // LIBOR market-model caplet, one-factor Euler (models.py:271-293).  The S
-// forward rates live in registers, held as y_n = delta L_n: the reference's
-// rate-step (dl = delta L_n; drift += sigma^2 dl / (1 + dl); L_n *= 1 +
-// drift delta + shock) becomes acc += y_n / (1 + y_n); y_n *= 1 + acc
-// sigma^2 delta + shock, one multiply fewer per rate-step (6 FP64 + MUFU).
+// forward rates live in registers, held as z_n = k delta L_n with k =
+// sigma^2 delta: the reference's rate-step (dl = delta L_n; drift +=
+// sigma^2 dl / (1 + dl); L_n *= 1 + drift delta + shock) becomes
+// f += z_n / (1 + z_n / k); z_n *= f, with f = 1 + shock at the step's start:
+// 5 FP64 + MUFU per rate-step instead of 7 (see libor_state_scale).
 // For S <= CHUNK the whole step/rate
 // triangle is unrolled; above that the step loop is dynamic and the rate
 // loop unrolled with uniform guards.  1/(1 + delta L) in the drift uses a
@@ -1466,13 +1477,14 @@ struct ModelLibor {
     if (n < NS) return Ls[n * TILE + threadIdx.x];
     return L[n - NS];
   }
-  double s2d, ssq, dstrike, ff;
+  double cz, ssq, dstrike, ff;
   __device__ void init(const ModelParams &mp_, Shared &s) {
-    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.delta * mp_.table[n];
+    const double kz = libor_state_scale(mp_);
+    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = kz * (mp_.delta * mp_.table[n]);
     sh = &s;
+    cz = 1.0 / kz;
     dstrike = mp_.delta * mp_.strike;
     ff = mp_.front_factor;
-    s2d = mp_.sigma * mp_.sigma * mp_.delta;
     ssq = mp_.sigma * sqrt(mp_.delta);
   }
   __device__ void begin() {
@@ -1481,14 +1493,13 @@ struct ModelLibor {
   }
   // static step (S <= CHUNK: whole triangle unrolled, i compile-time)
   __device__ __forceinline__ void step(int i, double z) {
-    const double g1 = fma(ssq, z, 1.0);
-    double acc = 0.0;
+    double f = fma(ssq, z, 1.0);
 #pragma unroll
     for (int n = 0; n < S; n++) {
       if (n >= i) {
-        double r = rcp1(1.0 + Lr(n));
-        acc = fma(Lr(n), r, acc);
-        Lr(n) *= fma(acc, s2d, g1);
+        double r = rcp1(fma(cz, Lr(n), 1.0));
+        f = fma(Lr(n), r, f);
+        Lr(n) *= f;
       }
     }
   }
@@ -1497,35 +1508,34 @@ struct ModelLibor {
   // code whose GRP reciprocals overlap; only the first alive group is
   // partial and masks its dead rates with selects.
   static constexpr int GRP = S % 8 == 0 ? 8 : (S % 4 == 0 ? 4 : (S % 5 == 0 ? 5 : 1));
-  __device__ __forceinline__ void group(int g, int i, double g1, double &drift, bool partial) {
+  __device__ __forceinline__ void group(int g, int i, double &f, bool partial) {
     double r[GRP];
 #pragma unroll
-    for (int k = 0; k < GRP; k++) r[k] = rcp1(1.0 + Lr(g * GRP + k));
+    for (int k = 0; k < GRP; k++) r[k] = rcp1(fma(cz, Lr(g * GRP + k), 1.0));
 #pragma unroll
     for (int k = 0; k < GRP; k++) {
       const int n = g * GRP + k;
       const double ln0 = Lr(n);
-      const double dn = fma(ln0, r[k], drift);
-      const double ln = ln0 * fma(dn, s2d, g1);
+      const double fn = fma(ln0, r[k], f);
+      const double ln = ln0 * fn;
       if (partial) {
         const bool alive = n >= i;
-        drift = alive ? dn : drift;
+        f = alive ? fn : f;
         Lr(n) = alive ? ln : ln0;
       } else {
-        drift = dn;
+        f = fn;
         Lr(n) = ln;
       }
     }
   }
   __device__ __forceinline__ void step_dyn(int i, double z) {
     static_assert(S % GRP == 0, "S must be a multiple of the rate group");
-    const double g1 = fma(ssq, z, 1.0);
-    double drift = 0.0;
+    double f = fma(ssq, z, 1.0);
     const int first = i / GRP;
 #pragma unroll
     for (int g = 0; g < S / GRP; g++) {
-      if (g == first) group(g, i, g1, drift, true);
-      else if (g > first) group(g, i, g1, drift, false);
+      if (g == first) group(g, i, f, true);
+      else if (g > first) group(g, i, f, false);
     }
   }
   __device__ void chunk(int d0, int Dc, const double *zcol) {
@@ -1539,10 +1549,10 @@ struct ModelLibor {
   __device__ double payoff() const {
     double prod = 1.0;
 #pragma unroll
-    for (int n = 0; n < S - 1; n++) prod *= 1.0 + Lv(n);
+    for (int n = 0; n < S - 1; n++) prod *= fma(cz, Lv(n), 1.0);
     const double lt = Lv(S - 1);
-    const double pay = fmax(lt - dstrike, 0.0);
-    return pay * ff * rcp2((1.0 + lt) * prod);
+    const double pay = fmax(fma(cz, lt, -dstrike), 0.0);
+    return pay * ff * rcp2(fma(cz, lt, 1.0) * prod);
   }
 };
 
@@ -1564,15 +1574,16 @@ struct ModelLiborDyn {
   const Shared *sh;
   double *Ls;
   int S;
-  double s2d, ssq, dstrike, ff;
+  double cz, ssq, dstrike, ff;
   __device__ void set_dyn(double *p) { Ls = p; }
   __device__ void init(const ModelParams &mp_, Shared &s) {
     S = mp_.dim;
-    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = mp_.delta * mp_.table[n];
+    const double kz = libor_state_scale(mp_);
+    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = kz * (mp_.delta * mp_.table[n]);
     sh = &s;
+    cz = 1.0 / kz;
     dstrike = mp_.delta * mp_.strike;
     ff = mp_.front_factor;
-    s2d = mp_.sigma * mp_.sigma * mp_.delta;
     ssq = mp_.sigma * sqrt(mp_.delta);
   }
   __device__ void begin() {
@@ -1582,24 +1593,24 @@ struct ModelLiborDyn {
     for (int k = 0; k < Dc; k++) {
       const int i = d0 + k;
       const double g1 = fma(ssq, zcol[k * TILE], 1.0);
-      double acc = 0.0;
+      double f = g1;
       double *L = Ls + threadIdx.x;
 #pragma unroll 4
       for (int n = i; n < S; n++) {
         const double ln = L[n * TILE];
-        const double r = rcp1(1.0 + ln);
-        acc = fma(ln, r, acc);
-        L[n * TILE] = ln * fma(acc, s2d, g1);
+        const double r = rcp1(fma(cz, ln, 1.0));
+        f = fma(ln, r, f);
+        L[n * TILE] = ln * f;
       }
     }
   }
   __device__ double payoff() const {
     const double *L = Ls + threadIdx.x;
     double prod = 1.0;
-    for (int n = 0; n < S - 1; n++) prod *= 1.0 + L[n * TILE];
+    for (int n = 0; n < S - 1; n++) prod *= fma(cz, L[n * TILE], 1.0);
     const double lt = L[(S - 1) * TILE];
-    const double pay = fmax(lt - dstrike, 0.0);
-    return pay * ff * rcp2((1.0 + lt) * prod);
+    const double pay = fmax(fma(cz, lt, -dstrike), 0.0);
+    return pay * ff * rcp2(fma(cz, lt, 1.0) * prod);
   }
 };
 
@@ -1935,7 +1946,7 @@ __global__ void __launch_bounds__(TILE, (Mdl::MINB < MaxBlocks<G>::value ? Mdl::
 // Consecutive rows use the tiled generators, explicit indices the direct.
 // ======================================================================
 template <class G>
-__global__ void __launch_bounds__(TILE) k_points(RepTables t, int rl, int64_t first,
+__global__ void __launch_bounds__(TILE, 4) k_points(RepTables t, int rl, int64_t first,
                                                  const int64_t *idx, int64_t count,
                                                  double *out) {
   extern __shared__ __align__(16) double zt[];  // ZT_BYTES

@@ -405,6 +405,22 @@ def test_libor_any_steps_vs_oracle(P, oracle, mat, acc):
     assert (np.abs(got - ref) <= 10 * PAYOFF_RTOL * scale).all()
 
 
+@pytest.mark.parametrize("sigma,mat,acc", [(0.0, 5.0, 0.25), (1e-160, 5.0, 0.25), (0.5, 5.0, 0.25),
+                                           (0.04, 3.0, 0.3), (0.2, 20.0, 0.25)])
+def test_libor_volatility_edges_vs_oracle(P, oracle, sigma, mat, acc):
+    """The kernels hold the rates as z = sigma^2 delta * delta L (the drift
+    weight folded in, scale clamped at 2^-900): sigma = 0 and tiny sigma
+    (no drift), a large sigma, a non-dyadic accrual (delta L rounded)."""
+    from paper_1408_5526_b200 import models as M
+    from paper_1408_5526_b200.harness import estimate_replications
+
+    model = M.LiborModel(M.LiborConfig(maturity=mat, accrual=acc, sigma=sigma))
+    for gen in ("rasrap-recursive", "philox"):
+        got = estimate_replications(gen, model, SEED, 3, 2, (2000,))
+        ref = _oracle_theta(oracle, gen, model, SEED, 3, 2, (2000,))
+        assert (np.abs(got - ref) <= THETA_RTOL * np.abs(ref)).all(), gen
+
+
 @pytest.mark.parametrize("cfg", [dict(months=24), dict(months=360, variance=0.0),
                                  dict(months=100, variance=0.0009, initial_rate=0.01)])
 def test_mbs_variants_vs_oracle(P, oracle, cfg):
