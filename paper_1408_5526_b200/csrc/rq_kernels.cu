@@ -1649,10 +1649,13 @@ __device__ __forceinline__ double atan_mbs(double y) {
   return fma(t * t2, p, t) + (hi ? c_atan_ctr[3] : c_atan_ctr[2]);
 }
 
-// MBS present value (models.py:430-449), monthly steps.  State: discount
-// disc, R = payment * remaining (so the cash flow is one product), the rate
-// and 1 - w of the previous month (1.0 before month 1: R * 1.0 is exact, as
-// the reference's skipped update).
+// MBS present value (models.py:430-449), monthly steps.  State: R =
+// payment * remaining (so the cash flow is one product), the rate, 1 - w of
+// the previous month (1.0 before month 1: R * 1.0 is exact, as the
+// reference's skipped update), and the present value as a fraction N / P:
+// the reference's discount disc_k = 1 / P_k with P_k = prod_{j<=k} (1 +
+// i_{j-1}), so pv_k = pv_{k-1} + a_k / P_k is N_k = N_{k-1} (1 + i_{k-1}) +
+// a_k over P_k, and the 360 divisions become one per path.
 struct ModelMbs {
   static constexpr bool NORMALS = true;
   static constexpr bool SMALL_LIBOR = false;
@@ -1664,7 +1667,7 @@ struct ModelMbs {
   double i0, sxi, k0, k1, k2, k3, k4, pay;
   uint32_t zlim_hi;  // high word of exp_zlim: |z| below it stays in the series range
   double ec[MBS_EXP_TERMS];
-  double disc, R, rate, omw, pv;
+  double P, R, rate, omw, N;
   __device__ void init(const ModelParams &mp_, Shared &) {
     ck = mp_.table;  // annuity ratios: uniform across the warp, L1-resident
     i0 = mp_.i0;
@@ -1680,11 +1683,11 @@ struct ModelMbs {
     for (int k = 0; k < MBS_EXP_TERMS; k++) ec[k] = mp_.ecoef[k];
   }
   __device__ void begin() {
-    disc = 1.0;
+    P = 1.0;
     R = pay;
     rate = i0;
     omw = 1.0;
-    pv = 0.0;
+    N = 0.0;
   }
   __device__ __forceinline__ double kexp(double z) const {  // k0 * exp(sigma_xi z)
     if (abs_hi(z) >= zlim_hi) return kexp_slow(k0, sxi, z);
@@ -1696,45 +1699,43 @@ struct ModelMbs {
   // Months in groups of MG: the shocks' exponentials, the discount
   // reciprocals and the prepayment arctangents of a group are independent
   // once the (cheap, serial) rate product is known, so they are issued
-  // together; only disc / R / pv remain serial (models.py:437-448).
+  // together; only P / R / N remain serial (models.py:437-448).
   static constexpr int MG = RQ_MBS_MG;
   __device__ void chunk(int d0, int Dc, const double *zcol) {
     int kk = 0;
     for (; kk + MG <= Dc; kk += MG) {
-      double e[MG], inv[MG], w[MG];
+      double e[MG], u[MG], w[MG];
 #pragma unroll
       for (int m = 0; m < MG; m++) e[m] = kexp(zcol[(kk + m) * TILE]);
       double r = rate;
 #pragma unroll
       for (int m = 0; m < MG; m++) {
-        inv[m] = 1.0 + r;  // u_k uses the rate before this month's update
+        u[m] = 1.0 + r;  // the discount uses the rate before this month's update
         r = e[m] * r;
         w[m] = r;
       }
 #pragma unroll
-      for (int m = 0; m < MG; m++) {
-        inv[m] = rcp2(inv[m]);
-        w[m] = fma(k2, atan_mbs(fma(k3, w[m], k4)), k1);
-      }
+      for (int m = 0; m < MG; m++) w[m] = fma(k2, atan_mbs(fma(k3, w[m], k4)), k1);
 #pragma unroll
       for (int m = 0; m < MG; m++) {
-        disc *= inv[m];
+        P *= u[m];
         R *= omw;
         omw = 1.0 - w[m];
-        pv = fma(disc * R, fma(w[m], __ldg(ck + d0 + kk + m), omw), pv);
+        N = fma(N, u[m], R * fma(w[m], __ldg(ck + d0 + kk + m), omw));
       }
       rate = r;
     }
     for (; kk < Dc; kk++) {
-      disc *= rcp2(1.0 + rate);
+      const double u = 1.0 + rate;
+      P *= u;
       R *= omw;
       rate = kexp(zcol[kk * TILE]) * rate;
       const double w = fma(k2, atan_mbs(fma(k3, rate, k4)), k1);
       omw = 1.0 - w;
-      pv = fma(disc * R, fma(w, __ldg(ck + d0 + kk), omw), pv);
+      N = fma(N, u, R * fma(w, __ldg(ck + d0 + kk), omw));
     }
   }
-  __device__ double payoff() const { return pv; }
+  __device__ double payoff() const { return N / P; }
 };
 
 // f = x_1 (FirstCoordinateModel, models.py:489-498) and f = 1 (ConstantModel).
