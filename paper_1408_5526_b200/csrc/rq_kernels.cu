@@ -1381,21 +1381,21 @@ struct GenKakutani {
 // == order of their bit patterns); four inputs are in flight per pass for
 // ILP; the ~9% tail inputs are queued and evaluated 32 at a time.
 // ======================================================================
-template <int FIXED = 0>  // FIXED > 0: Dc == FIXED known at compile time (no guards)
+template <int FIXED = 0, bool UNROLL = false>  // FIXED > 0: Dc == FIXED known at compile time
 __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *q) {
   const int Dc = FIXED > 0 ? FIXED : Dc_;
+  constexpr bool FULL = FIXED > 0 && FIXED % 4 == 0;  // no partial pass: no guards
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   int qn = 0;
-#pragma unroll
-  for (int d4 = 0; d4 < Dc; d4 += 4) {
+  auto pass = [&](int d4) {
     double p[4], x[4];
     bool tail[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       const int dd = d4 + k;
-      p[k] = dd < Dc ? zt[dd * TILE + threadIdx.x] : 0.5;
-      tail[k] = dd < Dc && invn_tail_p(p[k]);
+      p[k] = FULL || dd < Dc ? zt[dd * TILE + threadIdx.x] : 0.5;
+      tail[k] = (FULL || dd < Dc) && invn_tail_p(p[k]);
     }
 #pragma unroll
     for (int k = 0; k < 4; k++) x[k] = invn_central_q(p[k] - 0.5);
@@ -1405,9 +1405,21 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *
       const int slot = dd * TILE + threadIdx.x;
       unsigned b = __ballot_sync(0xffffffffu, tail[k]);
       if (tail[k]) q[qn + __popc(b & lt)] = (uint16_t)slot;
-      else if (dd < Dc) zt[slot] = x[k];
+      else if (FULL || dd < Dc) zt[slot] = x[k];
       qn += __popc(b);
     }
+  };
+  // A fixed-width chunk (single-chunk LIBOR) keeps one pass body: its path
+  // kernel is already long (the unrolled rate triangle), and instruction
+  // fetch, not the loop branch, is what costs there (measured: Philox /
+  // XORWOW C2 +5%); the persistent Rasrap kernel measured 0.7% better
+  // unrolled (UNROLL).
+  if constexpr (FIXED > 0 && !UNROLL) {
+#pragma unroll 1
+    for (int d4 = 0; d4 < Dc; d4 += 4) pass(d4);
+  } else {
+#pragma unroll
+    for (int d4 = 0; d4 < Dc; d4 += 4) pass(d4);
   }
   __syncwarp();
   for (int k = lane; k < qn; k += 32) {
@@ -1848,7 +1860,9 @@ __global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathAr
       __syncthreads();
     }
     if (d0 == 0) md.begin();
-    if (Mdl::NORMALS) chunk_to_normals<FixedDims<Mdl>::value>(z, Dc, phs.tq[warp]);
+    if (Mdl::NORMALS)
+      chunk_to_normals<FixedDims<Mdl>::value, std::is_same<G, GenRasrapRecTile<true>>::value>(
+          z, Dc, phs.tq[warp]);
     md.chunk(d0, Dc, z + threadIdx.x);
     if (d0 + Dc >= gdims) {
       const int64_t path = base + threadIdx.x;
