@@ -2035,14 +2035,14 @@ __global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t np
 // Register form of the stream for per-thread generators (Philox, SFC64):
 // four coordinates at a time straight from the generator into the central
 // inverse normal and the sum, no tile round trip through shared memory;
-// only the ~9% tail inputs go to a per-warp queue (value + store slot),
-// evaluated 32 at a time whenever 32 are waiting.
-template <class G>
+// only the ~9% tail inputs go to a per-warp queue (value, and the store slot
+// when STORE), evaluated 32 at a time whenever 32 are waiting.
+template <class G, bool STORE>
 __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_t npoints,
                                                      double *block_sums, double *store) {
   constexpr int QCAP = 32 + 4 * 32;  // < 32 left over + one 4-coordinate group
   __shared__ double qv[WARPS][QCAP];
-  __shared__ int64_t qs[WARPS][QCAP];
+  __shared__ int64_t qs[STORE ? WARPS : 1][STORE ? QCAP : 1];
   __shared__ double red[WARPS];
   __shared__ typename G::Shared gsh;
   G g;
@@ -2056,7 +2056,7 @@ __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_
     const double x0 = invn_tail(invn_fold(qv[warp][i], &neg));
     const double x = neg ? -x0 : x0;
     acc += x;
-    if (store) store[qs[warp][i]] = x;
+    if constexpr (STORE) store[qs[warp][i]] = x;
   };
   for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < npoints; tb += (int64_t)gridDim.x * TILE) {
     const int64_t r = tb + threadIdx.x;
@@ -2065,9 +2065,10 @@ __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_
       double u[4], x[4];
       bool tail[4], use[4];
       g.quad(rl, (uint64_t)r, d0, u);
+      const bool whole = d0 + 4 <= t.dim;  // uniform
 #pragma unroll
       for (int k = 0; k < 4; k++) {
-        use[k] = ok && d0 + k < t.dim;
+        use[k] = ok && (whole || d0 + k < t.dim);
         tail[k] = use[k] && invn_tail_p(u[k]);
       }
 #pragma unroll
@@ -2076,24 +2077,27 @@ __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_
       for (int k = 0; k < 4; k++) {
         if (use[k] && !tail[k]) {
           acc += x[k];
-          if (store) store[r * t.dim + d0 + k] = x[k];
+          if constexpr (STORE) store[r * t.dim + d0 + k] = x[k];
         }
         const unsigned b = __ballot_sync(0xffffffffu, tail[k]);
         if (tail[k]) {
           const int i = qn + __popc(b & lt);
           qv[warp][i] = u[k];
-          qs[warp][i] = r * t.dim + d0 + k;
+          if constexpr (STORE) qs[warp][i] = r * t.dim + d0 + k;
         }
         qn += __popc(b);
       }
-      __syncwarp();
-      while (qn >= 32) {
-        tail_one(qn - 32 + lane);
-        qn -= 32;
+      if (qn >= 32) {
+        __syncwarp();
+        do {
+          tail_one(qn - 32 + lane);
+          qn -= 32;
+        } while (qn >= 32);
         __syncwarp();
       }
     }
   }
+  __syncwarp();
   if (lane < qn) tail_one(lane);
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) red[warp] = acc;
@@ -2549,11 +2553,19 @@ static cudaError_t stream_t(const RepTables &t, int rl, int64_t npoints, double 
   return cudaGetLastError();
 }
 
+template <class G>
+static cudaError_t stream_reg_t(const RepTables &t, int rl, int64_t npoints, double *sums,
+                                int nblocks, double *store, cudaStream_t s) {
+  if (store) k_stream_reg<G, true><<<nblocks, TILE, 0, s>>>(t, rl, npoints, sums, store);
+  else k_stream_reg<G, false><<<nblocks, TILE, 0, s>>>(t, rl, npoints, sums, nullptr);
+  return cudaGetLastError();
+}
+
 int stream_grid_blocks(const RepTables &t) {
   const int64_t big = (int64_t)1 << 30;
   switch (t.gen) {
-    case GEN_PHILOX: return persistent_blocks(k_stream_reg<GenPhilox>, big);
-    case GEN_SFC64: return persistent_blocks(k_stream_reg<GenSfc64>, big);
+    case GEN_PHILOX: return persistent_blocks(k_stream_reg<GenPhilox, true>, big);
+    case GEN_SFC64: return persistent_blocks(k_stream_reg<GenSfc64, true>, big);
   }
   ModelParams mp{};
   mp.kind = MODEL_X1;
@@ -2569,16 +2581,12 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
       return stream_t<GenRasrapRecTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_RASRAP_COUNTER:
       return stream_t<GenRasrapCounterTile>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_PHILOX:
-      k_stream_reg<GenPhilox><<<nblocks, TILE, 0, s>>>(t, rl, npoints, block_sums, store);
-      return cudaGetLastError();
+    case GEN_PHILOX: return stream_reg_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_SOBOL_GRAY:
       return stream_t<GenSobolTile<true>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_SOBOL_COUNTER:
       return stream_t<GenSobolTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
-    case GEN_SFC64:
-      k_stream_reg<GenSfc64><<<nblocks, TILE, 0, s>>>(t, rl, npoints, block_sums, store);
-      return cudaGetLastError();
+    case GEN_SFC64: return stream_reg_t<GenSfc64>(t, rl, npoints, block_sums, nblocks, store, s);
   }
   return cudaErrorInvalidValue;
 }
