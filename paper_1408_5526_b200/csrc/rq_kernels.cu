@@ -42,6 +42,9 @@
 #ifndef RQ_LIBOR_STATIC_MAX
 #define RQ_LIBOR_STATIC_MAX 20  // LIBOR steps up to which the rate triangle is fully unrolled
 #endif
+#ifndef RQ_RASRAP_MINB
+#define RQ_RASRAP_MINB 5  // CTAs per SM for the persistent Rasrap tile with LIBOR S <= 20
+#endif
 #ifndef RQ_MINB_SMALL
 #define RQ_MINB_SMALL 4  // CTAs per SM targeted for LIBOR S <= 20 (register budget)
 #endif
@@ -1671,7 +1674,7 @@ __device__ __forceinline__ double atan_mbs(double y) {
 struct ModelMbs {
   static constexpr bool NORMALS = true;
   static constexpr bool SMALL_LIBOR = false;
-  static constexpr int MINB = 4;  // CTAs/SM (7 fit at <= 72 registers: measured 5% slower)
+  static constexpr int MINB = 4;  // lower bound; 70 registers: 7 CTAs/SM run (measured best: 6 -2%, 5 -7%)
   static constexpr int MAXM = 1 << 20;
   using Shared = NoShared;
   static __host__ __device__ int gen_dims(int dim) { return dim; }
@@ -1800,7 +1803,7 @@ template <class G, class Mdl>
 struct PathsMinB {
   static constexpr int base = Mdl::MINB < MaxBlocks<G>::value ? Mdl::MINB : MaxBlocks<G>::value;
   static constexpr int value =
-      std::is_same<G, GenRasrapRecTile<true>>::value && Mdl::SMALL_LIBOR ? 5 : base;
+      std::is_same<G, GenRasrapRecTile<true>>::value && Mdl::SMALL_LIBOR ? RQ_RASRAP_MINB : base;
 };
 
 template <class G, class Mdl>
@@ -2241,6 +2244,12 @@ template <class K>
 static int persistent_blocks(K kernel, int64_t work, size_t dyn = 0) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TILE, dyn);
+  // RQ_BLOCKS_PER_SM: optional cap on the persistent CTAs per SM (tuning)
+  static const int cap = [] {
+    const char *e = getenv("RQ_BLOCKS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  if (cap > 0 && per_sm > cap) per_sm = cap;
   if (per_sm < 1) per_sm = 1;
   int64_t b = (int64_t)per_sm * sm_count();
   return (int)(work < b ? (work < 1 ? 1 : work) : b);

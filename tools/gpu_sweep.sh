@@ -17,7 +17,7 @@ cat gpurun_out/bench_reference.json >> gpurun_out/sweep.json
 python tools/bench_table.py gpurun_out/sweep.json
 python -c "import __graft_entry__ as g; g.smoke()"
 # ncu evidence for the headline kernels (one capture each) + launch list of the default bench
-P=gpurun_out/prof7; mkdir -p $P
+P=${P:-gpurun_out/prof8}; mkdir -p $P
 NCU="ncu --set full --clock-control none --import-source on"
 timeout 600 $NCU -k regex:k_paths -s 1 -c 1 -o $P/c2_rasrap -f python tools/profile_step.py --workload c2 --reps 16 > $P/c2.log 2>&1
 timeout 600 $NCU -k regex:k_paths -s 1 -c 1 -o $P/c3_mbs -f python tools/profile_step.py --workload c3 --reps 4 --n 262144 > $P/c3.log 2>&1
