@@ -184,7 +184,8 @@ union PhaseShared {
   uint16_t tq[WARPS][CHUNK * 32];
 };
 
-constexpr int SIGD_MAX = 1024;  // sigma entries staged as doubles (single-chunk dims)
+constexpr int SIGD_MAX = 640;  // sigma entries staged as doubles (single-chunk dims)
+static_assert(CHUNK == 20 && SIGD_MAX >= 639, "the first CHUNK primes sum to 639");
 
 struct RasrapTileShared {
   uint16_t bd[CHUNK][MAX_CAP];     // base-p digits of the tile base B = n0 + base
@@ -1994,7 +1995,7 @@ __global__ void __launch_bounds__(TILE, 4) k_points(RepTables t, int rl, int64_t
 // t.dim, fused inverse normal, consumed by a sum (and optionally stored).
 // ======================================================================
 template <class G>
-__global__ void __launch_bounds__(TILE) k_stream(RepTables t, int rl, int64_t npoints,
+__global__ void __launch_bounds__(TILE, 4) k_stream(RepTables t, int rl, int64_t npoints,
                                                  double *block_sums, double *store) {
   extern __shared__ __align__(16) double zt[];  // ZT_BYTES
   __shared__ PhaseShared phs;
