@@ -354,7 +354,7 @@ def run_ours(args) -> dict:
             "gpu_launches": launches,
             "clocks": clk,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline: N=1 runs only
             out["cpu_baseline"] = cpu_baseline(model, gen, N, args)
         if args.workload == "c2" and not use_dist and not args.reps:
             out["comparison"] = generator_comparison(model, M, N)
