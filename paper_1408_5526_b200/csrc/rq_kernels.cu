@@ -197,10 +197,13 @@ struct RasrapTileShared {
   uint64_t st_base[CHUNK];         // tile base the state belongs to
   int32_t soff[CHUNK];             // offset of sigma_d in sigd
 };
-// + the persistent partial sums and sigma of a single-chunk model's dims
-// staged as doubles
+// + the persistent partial sums of the chunk's dims
 struct RasrapTilePersistShared : RasrapTileShared {
   double P[CHUNK][MAX_CAP + 1];  // S_j(B), j = 0..cap
+};
+// + their sigma tables staged as doubles (single-chunk models: the first
+// CHUNK dims)
+struct RasrapTilePersistSigShared : RasrapTilePersistShared {
   double sigd[SIGD_MAX];
 };
 struct RasrapDirectShared {
@@ -312,10 +315,12 @@ struct GenRasrapRecDirect {
 // That is ~TILE * p/(p-1) node updates per tile and dim instead of
 // TILE * log_p(n) for independent per-point chains, with the same
 // operations in the same order as the reference (bit-identical).
-template <bool PERSIST>
+template <bool PERSIST, bool SIGSM = PERSIST>
 struct GenRasrapRecTile {
-  using Shared = typename std::conditional<PERSIST, RasrapTilePersistShared,
-                                           RasrapTileShared>::type;
+  using Shared = typename std::conditional<
+      PERSIST,
+      typename std::conditional<SIGSM, RasrapTilePersistSigShared, RasrapTilePersistShared>::type,
+      RasrapTileShared>::type;
   const RepTables *t;
   Shared *sh;
   PhaseShared *ph;  // level buffers (aliased with the tail queues, see PhaseShared)
@@ -323,9 +328,11 @@ struct GenRasrapRecTile {
   // of one CTA share a persistent stream state and the dims' sigma tables are
   // staged in shared memory as doubles (the first CHUNK primes sum to 639 <=
   // SIGD_MAX).  Compile-time, so the persistent kernel carries no stateless
-  // or global-sigma code (instruction-cache footprint).
+  // or global-sigma code (instruction-cache footprint).  PERSIST without
+  // SIGSM: the chunk-major stream (k_stream_chunks), a CTA owning one chunk
+  // of any dims over consecutive tiles, sigma read from global memory.
   static constexpr bool persist = PERSIST;
-  static constexpr bool sig_smem = PERSIST;
+  static constexpr bool sig_smem = SIGSM;
   __device__ void setup(const RepTables &t_, Shared &s, int = 0) {
     t = &t_;
     sh = &s;
@@ -414,7 +421,7 @@ struct GenRasrapRecTile {
     }
   }
   __device__ __forceinline__ const double *sigd_of(int dd) const {
-    if constexpr (PERSIST) return sh->sigd + sh->soff[dd];
+    if constexpr (SIGSM) return sh->sigd + sh->soff[dd];
     return nullptr;
   }
   // per-dim tile state (one lane per dim): digits of B, hB, level sizes, S_J
@@ -492,7 +499,7 @@ struct GenRasrapRecTile {
     for (int dd = warp; dd < Dc; dd += WARPS) {
       const HaltonDim &h = c_hdim[d0 + dd];
       const int o = h.sig_off - off0;
-      if constexpr (PERSIST)
+      if constexpr (SIGSM)
         for (int a = lane; a < h.base; a += 32) R.sigd[o + a] = (double)gsig[h.sig_off + a];
       if (lane == 0) R.soff[dd] = o;
     }
@@ -518,7 +525,7 @@ struct GenRasrapRecTile {
       const double *ini = gsum + h.sum_off;
       // weights in the constant bank (always so for a persistent single-chunk
       // model: its <= CHUNK dims use < CWTS weights)
-      const bool cw = PERSIST || h.sum_off + h.cap < CWTS;
+      const bool cw = SIGSM || h.sum_off + h.cap < CWTS;
       const double *w = g_wts + h.sum_off;
       const int J = R.J[dd], hB = R.hB[dd];
       double *prev = ph->lev[warp][0], *next = ph->lev[warp][1];
@@ -2036,6 +2043,70 @@ __global__ void __launch_bounds__(TILE, 4) k_stream(RepTables t, int rl, int64_t
   }
 }
 
+// Chunk-major stream for the Rasrap tile (s > CHUNK): a CTA works on one
+// chunk c of CHUNK dims -- c = its SM's id mod nchunk, so the CTAs sharing
+// an SM (and its L1) read the same chunk's sigma tables -- and takes runs of
+// STREAM_RUN consecutive tiles of that chunk from a per-chunk counter, over
+// which its generator state advances tile to tile (odometer + re-chain)
+// instead of being rebuilt from the digits of n0 + base per tile and dim.
+// Same points, same normals; only which CTA sums which (point, chunk).
+constexpr int STREAM_RUN = 32;
+template <class G>
+__global__ void __launch_bounds__(TILE, 4) k_stream_chunks(RepTables t, int rl, int64_t npoints,
+                                                           double *block_sums, double *store,
+                                                           unsigned long long *ctr) {
+  extern __shared__ __align__(16) double zt[];  // ZT_BYTES
+  __shared__ PhaseShared phs;
+  __shared__ typename G::Shared gsh;
+  __shared__ double red[WARPS];
+  __shared__ unsigned long long run0;
+  G g;
+  give_phase(g, phs);
+  const int warp = threadIdx.x >> 5;
+  const int nchunk = (t.dim + CHUNK - 1) / CHUNK;
+  uint32_t smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  const int64_t ntile = (npoints + TILE - 1) / TILE;
+  double acc = 0.0;
+  // own chunk first, then help the others (an SM count that is not a
+  // multiple of nchunk leaves some chunks with one SM fewer)
+  for (int k = 0; k < nchunk; k++) {
+  const int c = (int)((smid + (uint32_t)k) % (uint32_t)nchunk);
+  const int d0 = c * CHUNK, Dc = t.dim - d0 < CHUNK ? t.dim - d0 : CHUNK;
+  g.setup(t, gsh, t.dim);  // new dims: no state to advance
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) run0 = atomicAdd(ctr + c, (unsigned long long)STREAM_RUN);
+    __syncthreads();
+    const int64_t lo = (int64_t)run0;
+    if (lo >= ntile) break;
+    const int64_t hi = lo + STREAM_RUN < ntile ? lo + STREAM_RUN : ntile;
+    for (int64_t tile = lo; tile < hi; tile++) {
+      const int64_t tb = tile * TILE, r = tb + threadIdx.x;
+      g.unit(rl, (uint64_t)tb, (uint64_t)r, d0, Dc, zt);
+      __syncthreads();
+      chunk_to_normals(zt, Dc, phs.tq[warp]);
+      if (r < npoints) {
+        for (int dd = 0; dd < Dc; dd++) {
+          const double z = zt[dd * TILE + threadIdx.x];
+          acc += z;
+          if (store) store[r * t.dim + d0 + dd] = z;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sm = 0.0;
+    for (int k = 0; k < WARPS; k++) sm += red[k];
+    block_sums[blockIdx.x] = sm;
+  }
+}
+
 // Register form of the stream for per-thread generators (Philox, SFC64):
 // four coordinates at a time straight from the generator into the central
 // inverse normal and the sum, no tile round trip through shared memory;
@@ -2576,6 +2647,10 @@ int stream_grid_blocks(const RepTables &t) {
   switch (t.gen) {
     case GEN_PHILOX: return persistent_blocks(k_stream_reg<GenPhilox, true>, big);
     case GEN_SFC64: return persistent_blocks(k_stream_reg<GenSfc64, true>, big);
+    case GEN_RASRAP_RECURSIVE: {  // chunk-major
+      using K = GenRasrapRecTile<true, false>;
+      return persistent_blocks(k_stream_chunks<K>, big, prep_dyn(k_stream_chunks<K>, ZT_BYTES));
+    }
   }
   ModelParams mp{};
   mp.kind = MODEL_X1;
@@ -2587,8 +2662,19 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
                                   double *block_sums, int nblocks, double *store,
                                   cudaStream_t s) {
   switch (t.gen) {
-    case GEN_RASRAP_RECURSIVE:
-      return stream_t<GenRasrapRecTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_RASRAP_RECURSIVE: {
+      using K = GenRasrapRecTile<true, false>;
+      const int nchunk = (t.dim + CHUNK - 1) / CHUNK;
+      unsigned long long *ctr = nullptr;
+      cudaError_t e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long) * nchunk, s);
+      if (e != cudaSuccess) return e;
+      cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * nchunk, s);
+      size_t dyn = prep_dyn(k_stream_chunks<K>, ZT_BYTES);
+      k_stream_chunks<K><<<nblocks, TILE, dyn, s>>>(t, rl, npoints, block_sums, store, ctr);
+      e = cudaGetLastError();
+      cudaFreeAsync(ctr, s);
+      return e;
+    }
     case GEN_RASRAP_COUNTER:
       return stream_t<GenRasrapCounterTile>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_PHILOX: return stream_reg_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
