@@ -2050,7 +2050,10 @@ __global__ void __launch_bounds__(TILE, 4) k_stream(RepTables t, int rl, int64_t
 // which its generator state advances tile to tile (odometer + re-chain)
 // instead of being rebuilt from the digits of n0 + base per tile and dim.
 // Same points, same normals; only which CTA sums which (point, chunk).
-constexpr int STREAM_RUN = 32;
+#ifndef RQ_STREAM_RUN
+#define RQ_STREAM_RUN 32
+#endif
+constexpr int STREAM_RUN = RQ_STREAM_RUN;  // tiles per counter grab
 template <class G>
 __global__ void __launch_bounds__(TILE, 4) k_stream_chunks(RepTables t, int rl, int64_t npoints,
                                                            double *block_sums, double *store,
