@@ -312,7 +312,8 @@ def test_pairwise_sum_bit_exact(P, n):
 
 @pytest.mark.parametrize("gen", ["philox", "rasrap-recursive", "sfc64", "sobol-gray"])
 @pytest.mark.parametrize("dim,npts,keep", [(360, 3000, True), (360, 3001, False),
-                                           (7, 1000, True), (7, 999, False), (1, 77, False)])
+                                           (7, 1000, True), (7, 999, False), (1, 77, False),
+                                           (361, 700, True), (40, 20000, False)])
 def test_stream_normals_sum(P, oracle, gen, dim, npts, keep):
     """Config-4 stream kernel: sum of fused normals vs oracle (small sample),
     with and without the stored normals, ragged dims and point counts."""
