@@ -228,9 +228,19 @@ def run_ours(args) -> dict:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     use_dist = "RANK" in os.environ  # launched by torchrun (any world size)
+    # one GPU per rank over NCCL; with fewer GPUs than ranks (a multi-rank
+    # check of this script on a one-GPU box) ranks share devices and the
+    # gather runs over gloo from host copies
+    ndev = torch.cuda.device_count()
+    shared_dev = use_dist and ndev < world
+    local = local % ndev if shared_dev else local
     torch.cuda.set_device(local)
     if use_dist:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if shared_dev else "cuda"
     lib = _lib.lib()
     kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
     if args.reps:
@@ -242,7 +252,7 @@ def run_ours(args) -> dict:
     grid = (N,)
     first = 1 + rank * M  # weak scaling: each rank its own replication ids
     theta = torch.empty((M, 1), dtype=torch.float64, device="cuda")
-    gathered = [torch.empty_like(theta) for _ in range(world)]
+    gathered = [torch.empty((M, 1), dtype=torch.float64, device=coll_dev) for _ in range(world)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def barrier():
@@ -253,7 +263,7 @@ def run_ours(args) -> dict:
     def one_step():
         h, n, keep = device_step(gen_id, model, SEED, first, M, grid, theta, lib, C, _lib)
         if use_dist:  # the one collective: theta of every rank, once per step
-            dist.all_gather(gathered, theta)
+            dist.all_gather(gathered, theta if not shared_dev else theta.cpu())
         return h, n
 
     peak, peak_ms = _lib.fp64_peak()
@@ -278,7 +288,7 @@ def run_ours(args) -> dict:
         step_ms.append(a.elapsed_time(b))
     clk = clocks.stop()
     ms = float(np.mean(step_ms))
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
     if use_dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
@@ -305,7 +315,7 @@ def run_ours(args) -> dict:
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     tr = _lib.stats_get()
     ne = len(e2e_ms)
-    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device="cuda")
+    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=coll_dev)
     if use_dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = paths / (float(e2e_t.item()) * 1e-3)
@@ -329,7 +339,7 @@ def run_ours(args) -> dict:
             "config": {"workload": desc, "generator": gen, "M_per_gpu": M, "N": N,
                        "model": kind, "dim": model.dim,
                        "parallelism": f"replication-sharded x{world} (theta all-gathered once "
-                                      f"per step{' over NCCL' if use_dist else ''})",
+                                      f"per step{(' over gloo, ranks sharing ' + str(ndev) + ' GPU(s)' if shared_dev else ' over NCCL') if use_dist else ''})",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "roofline": {
                 "bound": "fp64",
