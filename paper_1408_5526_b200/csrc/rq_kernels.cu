@@ -33,6 +33,9 @@
 #include "rq_device.cuh"
 #include "rq_internal.h"
 
+#ifndef RQ_SOBOL_STREAM_REG
+#define RQ_SOBOL_STREAM_REG 1  // config-4 Sobol' stream in register form (k_stream_reg)
+#endif
 #ifndef RQ_MBS_MG
 #define RQ_MBS_MG 4  // MBS months evaluated together (ILP across months)
 #endif
@@ -836,6 +839,77 @@ struct GenSobolTile {
           zt[dd * TILE + tt] = sobol_u(sobol_word<GRAY>(vd, shp[d0 + dd], base + (uint64_t)tt));
       }
     }
+  }
+};
+
+// Register form of the Sobol' stream (config 4, k_stream_reg): thread t of
+// a 128-aligned tile B takes point B + t in every dim.  With the tile
+// algebra of GenSobolTile its word is H_d ^ L_d(c): H_d folds the shift and
+// the index bits >= 7 (formed once per tile and dim into shared memory by the
+// CTA), c = (bidx & 127) ^ g(t) is the thread's low 7 index bits for every
+// dim, and L_d(c) = T0_d[c & 15] ^ T1_d[c >> 4] are XORs of the direction
+// words of those bits, tabled once per CTA (24 words per dim).  Same words
+// as sobol_word, so the same uniforms; three shared loads per coordinate.
+template <bool GRAY>
+struct GenSobolStream {
+  static constexpr bool TILE_HOOK = true;
+  const RepTables *t;
+  const uint32_t *v, *shp;
+  uint32_t *T0, *T1, *H;
+  int dim, dpad;
+  uint32_t c0, c1;
+  using Shared = NoShared;
+  static __host__ __device__ size_t dyn_bytes(int dim) {
+    return (size_t)((dim + 3) & ~3) * (16 + 8 + 1) * sizeof(uint32_t);
+  }
+  __device__ void setup(const RepTables &t_, Shared &, int dim_) {
+    t = &t_;
+    dim = dim_;
+    dpad = (dim + 3) & ~3;
+    extern __shared__ __align__(16) uint32_t sob_sm[];
+    T0 = sob_sm;
+    T1 = T0 + dpad * 16;
+    H = T1 + dpad * 8;
+  }
+  // per-CTA tables of replication rl (caller syncs before the first tile)
+  __device__ void rep(int rl) {
+    v = t->sobol_v + (int64_t)rl * dim * SOBOL_BITS;
+    shp = t->sobol_shift + (int64_t)rl * dim;
+    for (int e = threadIdx.x; e < dpad * 16; e += TILE) {
+      const int d = e >> 4;
+      const uint32_t c = (uint32_t)e & 15u;
+      uint32_t x = 0;
+      if (d < dim)
+        for (int k = 0; k < 4; k++) x ^= (c >> k) & 1u ? __ldg(v + d * SOBOL_BITS + k) : 0u;
+      T0[e] = x;
+    }
+    for (int e = threadIdx.x; e < dpad * 8; e += TILE) {
+      const int d = e >> 3;
+      const uint32_t c = (uint32_t)e & 7u;
+      uint32_t x = 0;
+      if (d < dim)
+        for (int k = 0; k < 3; k++) x ^= (c >> k) & 1u ? __ldg(v + d * SOBOL_BITS + 4 + k) : 0u;
+      T1[e] = x;
+    }
+  }
+  // tile base tb (multiple of TILE): H for every dim, this thread's c
+  __device__ void tile(uint64_t tb) {
+    __syncthreads();  // the previous tile's H reads are done
+    const uint64_t bidx = GRAY ? (tb ^ (tb >> 1)) : tb;
+    for (int d = threadIdx.x; d < dpad; d += TILE)
+      H[d] = d < dim ? sobol_word<false>(v + d * SOBOL_BITS, __ldg(shp + d), (bidx >> 7) << 7) : 0u;
+    const uint32_t l = threadIdx.x;
+    const uint32_t c = ((uint32_t)bidx & 127u) ^ (GRAY ? l ^ (l >> 1) : l);
+    c0 = c & 15u;
+    c1 = c >> 4;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void quad(int, uint64_t, int d0, double u[4]) {
+    const uint4 h = *reinterpret_cast<const uint4 *>(H + d0);
+    const uint32_t hh[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      u[k] = sobol_u(hh[k] ^ T0[(d0 + k) * 16 + c0] ^ T1[(d0 + k) * 8 + c1]);
   }
 };
 
@@ -2110,6 +2184,17 @@ __global__ void __launch_bounds__(TILE, 4) k_stream_chunks(RepTables t, int rl, 
   }
 }
 
+template <class G, class = void>
+struct HasTileHook : std::false_type {};
+template <class G>
+struct HasTileHook<G, std::void_t<decltype(G::TILE_HOOK)>> : std::true_type {};
+
+template <class G>
+static size_t stream_reg_dyn(int dim) {
+  if constexpr (HasTileHook<G>::value) return G::dyn_bytes(dim);
+  else return 0;
+}
+
 // Register form of the stream for per-thread generators (Philox, SFC64):
 // four coordinates at a time straight from the generator into the central
 // inverse normal and the sum, no tile round trip through shared memory;
@@ -2125,6 +2210,7 @@ __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_
   __shared__ typename G::Shared gsh;
   G g;
   g.setup(t, gsh, t.dim);
+  if constexpr (HasTileHook<G>::value) g.rep(rl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   double acc = 0.0;
@@ -2137,6 +2223,7 @@ __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_
     if constexpr (STORE) store[qs[warp][i]] = x;
   };
   for (int64_t tb = (int64_t)blockIdx.x * TILE; tb < npoints; tb += (int64_t)gridDim.x * TILE) {
+    if constexpr (HasTileHook<G>::value) g.tile((uint64_t)tb);
     const int64_t r = tb + threadIdx.x;
     const bool ok = r < npoints;
     for (int d0 = 0; d0 < t.dim; d0 += 4) {
@@ -2640,8 +2727,14 @@ static cudaError_t stream_t(const RepTables &t, int rl, int64_t npoints, double 
 template <class G>
 static cudaError_t stream_reg_t(const RepTables &t, int rl, int64_t npoints, double *sums,
                                 int nblocks, double *store, cudaStream_t s) {
-  if (store) k_stream_reg<G, true><<<nblocks, TILE, 0, s>>>(t, rl, npoints, sums, store);
-  else k_stream_reg<G, false><<<nblocks, TILE, 0, s>>>(t, rl, npoints, sums, nullptr);
+  const size_t dyn = stream_reg_dyn<G>(t.dim);
+  if (store) {
+    if (dyn) prep_dyn(k_stream_reg<G, true>, dyn);
+    k_stream_reg<G, true><<<nblocks, TILE, dyn, s>>>(t, rl, npoints, sums, store);
+  } else {
+    if (dyn) prep_dyn(k_stream_reg<G, false>, dyn);
+    k_stream_reg<G, false><<<nblocks, TILE, dyn, s>>>(t, rl, npoints, sums, nullptr);
+  }
   return cudaGetLastError();
 }
 
@@ -2650,6 +2743,16 @@ int stream_grid_blocks(const RepTables &t) {
   switch (t.gen) {
     case GEN_PHILOX: return persistent_blocks(k_stream_reg<GenPhilox, true>, big);
     case GEN_SFC64: return persistent_blocks(k_stream_reg<GenSfc64, true>, big);
+#if RQ_SOBOL_STREAM_REG
+    case GEN_SOBOL_GRAY:
+      return persistent_blocks(k_stream_reg<GenSobolStream<true>, true>, big,
+                               prep_dyn(k_stream_reg<GenSobolStream<true>, true>,
+                                        GenSobolStream<true>::dyn_bytes(t.dim)));
+    case GEN_SOBOL_COUNTER:
+      return persistent_blocks(k_stream_reg<GenSobolStream<false>, true>, big,
+                               prep_dyn(k_stream_reg<GenSobolStream<false>, true>,
+                                        GenSobolStream<false>::dyn_bytes(t.dim)));
+#endif
     case GEN_RASRAP_RECURSIVE: {  // chunk-major
       using K = GenRasrapRecTile<true, false>;
       return persistent_blocks(k_stream_chunks<K>, big, prep_dyn(k_stream_chunks<K>, ZT_BYTES));
@@ -2681,10 +2784,17 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
     case GEN_RASRAP_COUNTER:
       return stream_t<GenRasrapCounterTile>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_PHILOX: return stream_reg_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
+#if RQ_SOBOL_STREAM_REG
+    case GEN_SOBOL_GRAY:
+      return stream_reg_t<GenSobolStream<true>>(t, rl, npoints, block_sums, nblocks, store, s);
+    case GEN_SOBOL_COUNTER:
+      return stream_reg_t<GenSobolStream<false>>(t, rl, npoints, block_sums, nblocks, store, s);
+#else
     case GEN_SOBOL_GRAY:
       return stream_t<GenSobolTile<true>>(t, rl, npoints, block_sums, nblocks, store, s);
     case GEN_SOBOL_COUNTER:
       return stream_t<GenSobolTile<false>>(t, rl, npoints, block_sums, nblocks, store, s);
+#endif
     case GEN_SFC64: return stream_reg_t<GenSfc64>(t, rl, npoints, block_sums, nblocks, store, s);
   }
   return cudaErrorInvalidValue;

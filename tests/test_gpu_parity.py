@@ -310,7 +310,7 @@ def test_pairwise_sum_bit_exact(P, n):
     assert float(out.item()) == np.sum(a)
 
 
-@pytest.mark.parametrize("gen", ["philox", "rasrap-recursive", "sfc64", "sobol-gray"])
+@pytest.mark.parametrize("gen", ["philox", "rasrap-recursive", "sfc64", "sobol-gray", "sobol-counter"])
 @pytest.mark.parametrize("dim,npts,keep", [(360, 3000, True), (360, 3001, False),
                                            (7, 1000, True), (7, 999, False), (1, 77, False),
                                            (361, 700, True), (40, 20000, False)])
