@@ -36,6 +36,9 @@
 #ifndef RQ_SOBOL_STREAM_REG
 #define RQ_SOBOL_STREAM_REG 1  // config-4 Sobol' stream in register form (k_stream_reg)
 #endif
+#ifndef RQ_SOBOL_PERSIST
+#define RQ_SOBOL_PERSIST 1  // persistent Sobol' tile state for single-chunk models
+#endif
 #ifndef RQ_MBS_MG
 #define RQ_MBS_MG 4  // MBS months evaluated together (ILP across months)
 #endif
@@ -838,6 +841,100 @@ struct GenSobolTile {
         for (int tt = lane; tt < TILE; tt += 32)
           zt[dd * TILE + tt] = sobol_u(sobol_word<GRAY>(vd, shp[d0 + dd], base + (uint64_t)tt));
       }
+    }
+  }
+};
+
+// Persistent Sobol' tile (single-chunk models: a CTA prices contiguous
+// tiles, dispatch as for the persistent Rasrap tile).  The warp owning a
+// dim keeps, in shared memory, the tile's high word H_d (shift and index
+// bits >= 7) and per-replication tables of the low seven bits: T0_d[16] and
+// T1_d[8] (XORs of direction words 0-3 and 4-6) and the three warp-uniform
+// point offsets of GenSobolTile.  From tile T-1 to T the high (Gray) index
+// changes by g(T) ^ g(T-1) = 1 << ctz(T) (counter order: the bits of
+// T ^ (T-1)), so H_d takes one XOR per tile instead of a loop over the set
+// bits of the index; each lane's word is H_d ^ T0_d[c & 15] ^ T1_d[c >> 4].
+// Same words as sobol_word (checked by the points / theta tests).
+struct SobolPersistShared {
+  uint32_t H[CHUNK];
+  uint32_t T0[CHUNK][16];
+  uint32_t T1[CHUNK][8];
+  uint32_t W[CHUNK][4];  // 0, w1, w2, w3
+  int32_t st_rl[WARPS];
+  uint32_t st_T[WARPS];
+};
+template <bool GRAY>
+struct GenSobolTileP {
+  const RepTables *t;
+  SobolPersistShared *sh;
+  using Shared = SobolPersistShared;
+  __device__ void setup(const RepTables &t_, Shared &s, int = 0) {
+    t = &t_;
+    sh = &s;
+    for (int k = threadIdx.x; k < WARPS; k += TILE) s.st_rl[k] = -1;
+  }
+  __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
+    Shared &R = *sh;
+    const uint32_t *v = t->sobol_v + (int64_t)rl * t->dim * SOBOL_BITS;
+    const uint32_t *shp = t->sobol_shift + (int64_t)rl * t->dim;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t T = (uint32_t)(base >> 7);  // base is tile-aligned; indices < 2^32
+    const uint32_t gT = GRAY ? T ^ (T >> 1) : T;
+    if (R.st_rl[warp] != rl) {  // new replication: tables and H of the warp's dims
+#pragma unroll 1
+      for (int dd = warp; dd < Dc; dd += WARPS) {
+        const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS;
+        uint32_t x = 0;
+        if (lane < 16) {
+#pragma unroll
+          for (int k = 0; k < 4; k++) x ^= (lane >> k) & 1 ? __ldg(vd + k) : 0u;
+          R.T0[dd][lane] = x;
+        } else if (lane < 24) {
+#pragma unroll
+          for (int k = 0; k < 3; k++) x ^= ((lane - 16) >> k) & 1 ? __ldg(vd + 4 + k) : 0u;
+          R.T1[dd][lane - 16] = x;
+        } else if (lane < 28) {
+          const uint32_t v4 = __ldg(vd + 4), v5 = __ldg(vd + 5), v6 = __ldg(vd + 6);
+          const int m = lane - 24;
+          x = m == 0 ? 0u
+              : m == 1 ? (GRAY ? v4 ^ v5 : v5)
+              : m == 2 ? (GRAY ? v5 ^ v6 : v6)
+                       : (GRAY ? v4 ^ v6 : v5 ^ v6);
+          R.W[dd][m] = x;
+        } else if (lane == 28) {
+          R.H[dd] = sobol_word<false>(vd, __ldg(shp + d0 + dd), (uint64_t)gT << 7);
+        }
+      }
+    } else if (T == R.st_T[warp] + 1u) {  // next tile: XOR in the changed high bits
+      const uint32_t chg = GRAY ? (T & (0u - T)) : (T ^ (T - 1u));
+#pragma unroll 1
+      for (int dd = warp + lane * WARPS; dd < Dc; dd += 32 * WARPS) {
+        const uint32_t *vd = v + (d0 + dd) * SOBOL_BITS + 7;
+        uint32_t x = R.H[dd];
+        for (uint32_t b = chg; b; b &= b - 1u) x ^= __ldg(vd + __ffs(b) - 1);
+        R.H[dd] = x;
+      }
+    } else {  // a jump (first tile of the CTA in this replication)
+#pragma unroll 1
+      for (int dd = warp + lane * WARPS; dd < Dc; dd += 32 * WARPS)
+        R.H[dd] = sobol_word<false>(v + (d0 + dd) * SOBOL_BITS, __ldg(shp + d0 + dd),
+                                    (uint64_t)gT << 7);
+    }
+    if (lane == 0) {
+      R.st_rl[warp] = rl;
+      R.st_T[warp] = T;
+    }
+    __syncwarp();
+    const uint32_t c = (GRAY ? (T & 1u) << 6 : 0u) ^ (GRAY ? (uint32_t)(lane ^ (lane >> 1)) : (uint32_t)lane);
+    const uint32_t c0 = c & 15u, c1 = c >> 4;
+#pragma unroll 1
+    for (int dd = warp; dd < Dc; dd += WARPS) {
+      const uint32_t x = R.H[dd] ^ R.T0[dd][c0] ^ R.T1[dd][c1];
+      double *row = zt + dd * TILE + lane;
+      row[0] = sobol_u(x);
+      row[32] = sobol_u(x ^ R.W[dd][1]);
+      row[64] = sobol_u(x ^ R.W[dd][2]);
+      row[96] = sobol_u(x ^ R.W[dd][3]);
     }
   }
 };
@@ -2515,8 +2612,19 @@ static cudaError_t paths_dispatch(const PathArgs &a, int *launched, cudaStream_t
                  : paths_g<GenRasrapRecTile<true>>(a, launched, s, probe, blocks);
     case GEN_RASRAP_COUNTER: return paths_g<GenRasrapCounterTile>(a, launched, s, probe, blocks);
     case GEN_PHILOX: return paths_g<GenPhilox>(a, launched, s, probe, blocks);
+#if RQ_SOBOL_PERSIST
+    case GEN_SOBOL_GRAY:
+      return a.mp.kind == MODEL_MBS || a.mp.dim > CHUNK
+                 ? paths_g<GenSobolTile<true>>(a, launched, s, probe, blocks)
+                 : paths_g<GenSobolTileP<true>>(a, launched, s, probe, blocks);
+    case GEN_SOBOL_COUNTER:
+      return a.mp.kind == MODEL_MBS || a.mp.dim > CHUNK
+                 ? paths_g<GenSobolTile<false>>(a, launched, s, probe, blocks)
+                 : paths_g<GenSobolTileP<false>>(a, launched, s, probe, blocks);
+#else
     case GEN_SOBOL_GRAY: return paths_g<GenSobolTile<true>>(a, launched, s, probe, blocks);
     case GEN_SOBOL_COUNTER: return paths_g<GenSobolTile<false>>(a, launched, s, probe, blocks);
+#endif
     case GEN_SFC64: return paths_g<GenSfc64>(a, launched, s, probe, blocks);
   }
   return cudaErrorInvalidValue;

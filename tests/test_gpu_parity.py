@@ -291,10 +291,14 @@ def test_x1_theta_bit_exact_large(P, oracle):
 
     model = M.FirstCoordinateModel()
     grid = (999_983, 2**20)
-    for gen in ("rasrap-recursive", "philox"):
+    from paper_1408_5526_b200.tables import sobol_directions
+
+    sob = sobol_directions(model.dim)
+    for gen in ("rasrap-recursive", "philox", "sobol-gray", "sobol-counter"):
         got = estimate_replications(gen, model, SEED, 1, 3, grid)
-        ref = oracle.run_replications(gen, model, SEED, 1, 3, grid, threads=3)
-        assert np.array_equal(got, ref)
+        ref = oracle.run_replications(gen, model, SEED, 1, 3, grid, threads=3,
+                                      sobol_v=sob if gen.startswith("sobol") else None)
+        assert np.array_equal(got, ref), gen
 
 
 @pytest.mark.parametrize("n", [1, 7, 8, 127, 128, 129, 1000, 10_000, 2**20, 10**6 + 3])
