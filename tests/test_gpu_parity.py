@@ -384,7 +384,7 @@ def test_libor_steps_vs_oracle(P, oracle, mat, acc):
     from paper_1408_5526_b200.harness import estimate_replications
 
     model = M.LiborModel(M.LiborConfig(maturity=mat, accrual=acc))
-    for gen in ("rasrap-recursive", "philox"):
+    for gen in ("rasrap-recursive", "philox", "sobol-gray", "sobol-counter"):
         got = estimate_replications(gen, model, SEED, 5, 2, (3000,))
         ref = _oracle_theta(oracle, gen, model, SEED, 5, 2, (3000,))
         assert (np.abs(got / ref - 1)).max() <= THETA_RTOL
@@ -399,7 +399,7 @@ def test_libor_any_steps_vs_oracle(P, oracle, mat, acc):
     from paper_1408_5526_b200.harness import estimate_replications
 
     model = M.LiborModel(M.LiborConfig(maturity=mat, accrual=acc))
-    for gen in ("rasrap-recursive", "philox", "xorwow", "kakutani"):
+    for gen in ("rasrap-recursive", "philox", "xorwow", "kakutani", "sobol-gray", "sobol-counter"):
         got = estimate_replications(gen, model, SEED, 3, 2, (2000,))
         ref = _oracle_theta(oracle, gen, model, SEED, 3, 2, (2000,))
         # (S = 1: the caplet is out of the money on every path, theta == 0)
