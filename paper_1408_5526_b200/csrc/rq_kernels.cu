@@ -39,6 +39,9 @@
 #ifndef RQ_SOBOL_PERSIST
 #define RQ_SOBOL_PERSIST 1  // persistent Sobol' tile state for single-chunk models
 #endif
+#ifndef RQ_REDUCE_WARP
+#define RQ_REDUCE_WARP 1  // numpy pairwise leaves: eight lanes per leaf (coalesced)
+#endif
 #ifndef RQ_MBS_MG
 #define RQ_MBS_MG 4  // MBS months evaluated together (ILP across months)
 #endif
@@ -2436,8 +2439,32 @@ __global__ void k_reduce(SumPlan plan, const double *pay, int64_t pay_stride, do
   const int rep = blockIdx.y;
   const double *a = pay + (int64_t)rep * pay_stride;
   double *val = scratch + (int64_t)rep * plan.nnodes;
+#if RQ_REDUCE_WARP
+  {  // eight lanes per leaf: lane j carries numpy's accumulator r_j (elements
+     // j, j+8, ... in order), the fold ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by
+     // xor shuffles (each sum formed by the same two operands), lane 0 adds
+     // the n % 8 tail in order -- leaf_sum's arithmetic, coalesced loads
+    const int j = threadIdx.x & 7;
+    const int k = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 3);
+    const bool has = k < plan.nleaves;
+    const int n = has ? plan.leaf_len[k] : 0;
+    const double *b = a + (has ? plan.leaf_start[k] : 0);
+    const int m = n - n % 8;
+    double r = n >= 8 ? b[j] : 0.0;
+    for (int i = 8 + j; i < m; i += 8) r = dadd(r, b[i]);
+    r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = dadd(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (has && j == 0) {
+      double res = n >= 8 ? r : 0.0;
+      for (int i = m; i < n; i++) res = dadd(res, b[i]);
+      val[k] = res;
+    }
+  }
+#else
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < plan.nleaves) val[k] = leaf_sum(a + plan.leaf_start[k], plan.leaf_len[k]);
+#endif
   __shared__ bool last;
   __threadfence();
   __syncthreads();
@@ -2780,7 +2807,7 @@ cudaError_t launch_paths_seq(const RepTables &t, const ModelParams &mp, int rep_
 cudaError_t launch_reduce(const SumPlan &plan, const double *payoffs, int64_t pay_stride,
                           int reps, double *theta, int theta_stride, double *scratch,
                           unsigned *tickets, cudaStream_t s) {
-  dim3 grid((plan.nleaves + 255) / 256, reps);
+  dim3 grid((plan.nleaves + (RQ_REDUCE_WARP ? 31 : 255)) / (RQ_REDUCE_WARP ? 32 : 256), reps);
   k_reduce<<<grid, 256, 0, s>>>(plan, payoffs, pay_stride, theta, theta_stride, scratch,
                                 tickets);
   return cudaGetLastError();
