@@ -1566,8 +1566,11 @@ struct GenKakutani {
 // == order of their bit patterns); four inputs are in flight per pass for
 // ILP; the ~9% tail inputs are queued and evaluated 32 at a time.
 // ======================================================================
-template <int FIXED = 0, bool UNROLL = false>  // FIXED > 0: Dc == FIXED known at compile time
-__device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *q) {
+// SUM: the normals are only summed (config-4 stream without a store): each
+// goes into *acc where it is formed instead of back into the tile.
+template <int FIXED = 0, bool UNROLL = false, bool SUM = false>  // FIXED > 0: Dc == FIXED known at compile time
+__device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *q,
+                                                 double *acc = nullptr) {
   const int Dc = FIXED > 0 ? FIXED : Dc_;
   constexpr bool FULL = FIXED > 0 && FIXED % 4 == 0;  // no partial pass: no guards
   const int lane = threadIdx.x & 31;
@@ -1590,7 +1593,10 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *
       const int slot = dd * TILE + threadIdx.x;
       unsigned b = __ballot_sync(0xffffffffu, tail[k]);
       if (tail[k]) q[qn + __popc(b & lt)] = (uint16_t)slot;
-      else if (FULL || dd < Dc) zt[slot] = x[k];
+      else if (FULL || dd < Dc) {
+        if constexpr (SUM) *acc += x[k];
+        else zt[slot] = x[k];
+      }
       qn += __popc(b);
     }
   };
@@ -1612,7 +1618,8 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *
     bool neg;
     double pl = invn_fold(zt[slot], &neg);
     double x = invn_tail(pl);
-    zt[slot] = neg ? -x : x;
+    if constexpr (SUM) *acc += neg ? -x : x;
+    else zt[slot] = neg ? -x : x;
   }
   __syncwarp();
 }
@@ -2228,7 +2235,7 @@ __global__ void __launch_bounds__(TILE, 4) k_stream(RepTables t, int rl, int64_t
 #define RQ_STREAM_RUN 32
 #endif
 constexpr int STREAM_RUN = RQ_STREAM_RUN;  // tiles per counter grab
-template <class G>
+template <class G, bool STORE = true>
 __global__ void __launch_bounds__(TILE, 4) k_stream_chunks(RepTables t, int rl, int64_t npoints,
                                                            double *block_sums, double *store,
                                                            unsigned long long *ctr) {
@@ -2262,13 +2269,19 @@ __global__ void __launch_bounds__(TILE, 4) k_stream_chunks(RepTables t, int rl, 
       const int64_t tb = tile * TILE, r = tb + threadIdx.x;
       g.unit(rl, (uint64_t)tb, (uint64_t)r, d0, Dc, zt);
       __syncthreads();
-      chunk_to_normals(zt, Dc, phs.tq[warp]);
-      if (r < npoints) {
-        for (int dd = 0; dd < Dc; dd++) {
-          const double z = zt[dd * TILE + threadIdx.x];
-          acc += z;
-          if (store) store[r * t.dim + d0 + dd] = z;
+      if constexpr (STORE) {
+        chunk_to_normals(zt, Dc, phs.tq[warp]);
+        if (r < npoints) {
+          for (int dd = 0; dd < Dc; dd++) {
+            const double z = zt[dd * TILE + threadIdx.x];
+            acc += z;
+            store[r * t.dim + d0 + dd] = z;
+          }
         }
+      } else {
+        if (r >= npoints)  // points past the end: uniforms of 1/2 (normal 0)
+          for (int dd = 0; dd < Dc; dd++) zt[dd * TILE + threadIdx.x] = 0.5;
+        chunk_to_normals<0, false, true>(zt, Dc, phs.tq[warp], &acc);
       }
       __syncthreads();
     }
@@ -2910,8 +2923,15 @@ cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
       cudaError_t e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long) * nchunk, s);
       if (e != cudaSuccess) return e;
       cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * nchunk, s);
-      size_t dyn = prep_dyn(k_stream_chunks<K>, ZT_BYTES);
-      k_stream_chunks<K><<<nblocks, TILE, dyn, s>>>(t, rl, npoints, block_sums, store, ctr);
+      if (store) {
+        prep_dyn(k_stream_chunks<K, true>, ZT_BYTES);
+        k_stream_chunks<K, true><<<nblocks, TILE, ZT_BYTES, s>>>(t, rl, npoints, block_sums,
+                                                                 store, ctr);
+      } else {
+        prep_dyn(k_stream_chunks<K, false>, ZT_BYTES);
+        k_stream_chunks<K, false><<<nblocks, TILE, ZT_BYTES, s>>>(t, rl, npoints, block_sums,
+                                                                  nullptr, ctr);
+      }
       e = cudaGetLastError();
       cudaFreeAsync(ctr, s);
       return e;
