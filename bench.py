@@ -167,7 +167,9 @@ def run_stream(args) -> dict:
 
     from paper_1408_5526_b200 import _lib
 
-    torch.cuda.set_device(0)
+    if int(os.environ.get("RANK", "0")) != 0:  # a one-GPU stream: other ranks idle
+        return None
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count()))
     lib = _lib.lib()
     dim, npts = 360, WORKLOADS["c4"][4]
     if args.reps:
