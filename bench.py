@@ -1,21 +1,28 @@
 """Benchmark: RQMC paths/s of the fused B200 path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c3|c5|c1] [--generator NAME]
+                    [--workload c2|c3|c5|c1|c4] [--generator NAME]
 
-A step is one full run of the workload's replication loop on this rank
-(default C2: LIBOR caplet, 20 quarterly forwards, rasrap-recursive,
-M = 1024 replications x N = 2^20 paths): device randomisation setup, fused
-generator -> inverse normal -> Euler path -> payoff kernel, numpy-order
-reduction to theta.  Multi-GPU (torchrun, one process per GPU, NCCL) is
-weak scaling: every rank owns its own M replications (ids offset by rank),
+A step is one full run of the workload's replication loop (default C2:
+LIBOR caplet, 20 quarterly forwards, rasrap-recursive, M = 1024
+replications x N = 2^20 paths): device randomisation setup, fused generator
+-> inverse normal -> Euler path -> payoff kernel, numpy-order reduction to
+theta.  Multi-GPU (torchrun, one process per GPU, NCCL) is STRONG scaling,
+as the reference splits a fixed M over its workers (harness.py:349-358):
+rank r of W owns the contiguous replication ids distributed.shard(M, W, r),
 no data-path collective, theta all-gathered once per step; the time is the
-max over ranks.  Rank 0 prints one JSON line.
+max over ranks and `value` = M x N / that time.  The gathered theta is
+bit-identical for every W (`theta_sha16`).  Rank 0 prints one JSON line.
+
+The N=1 line carries `cpu_baseline` (the oracle timed on the host cores on
+`cores` replications of the same workload at full N) and `parity`: theta of
+those same replication ids -- the first and the last ids of the M range, so
+the last payoff batch is covered -- from the oracle against the GPU's.
 
 --impl reference times the CPU oracle (a bit-exact C restatement of the
 reference numba path, oracle/; the reference itself is Python+numba and has
 no compiled artefact to run here) on the host cores with all threads, on a
-bounded sample of the same workload.
+bounded sample of the same workload, plus a one-thread figure (`workers_1`).
 """
 
 from __future__ import annotations
@@ -216,14 +223,40 @@ def run_stream(args) -> dict:
     }
 
 
+def workload_config(args) -> tuple:
+    """(model, M, N, desc, config dict) -- the config dict is printed by BOTH
+    arms, identical, so the driver can match them."""
+    kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
+    if args.reps:
+        M = args.reps
+        desc += f" [M overridden to {M}]"
+    model = build_model(kind, mat, acc)
+    cfg = {"workload": desc, "generator": args.generator, "M": M, "N": N, "model": kind,
+           "dim": model.dim,
+           "l2": "GPU arm: L2 flushed between timed steps (256 MiB write); inputs are "
+                 "generated on chip"}
+    return model, M, N, desc, cfg
+
+
+def parity_ids(M: int, k: int):
+    """The first ceil(k/2) and the last floor(k/2) replication ids of 1..M."""
+    import numpy as np
+
+    k = max(1, min(k, M))
+    lo = (k + 1) // 2
+    return np.unique(np.r_[np.arange(1, lo + 1), np.arange(M - (k - lo) + 1, M + 1)])
+
+
 def run_ours(args) -> dict:
     import ctypes as C
+    import hashlib
 
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_1408_5526_b200 import _lib
+    from paper_1408_5526_b200.distributed import shard
     from paper_1408_5526_b200.harness import estimate_replications
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -244,17 +277,18 @@ def run_ours(args) -> dict:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     coll_dev = "cpu" if shared_dev else "cuda"
     lib = _lib.lib()
-    kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
-    if args.reps:
-        M = args.reps
-        desc += f" [M overridden to {M} per GPU]"
-    model = build_model(kind, mat, acc)
+    model, M, N, desc, cfg = workload_config(args)
     gen = args.generator
     gen_id = _lib.GEN_IDS[gen]
     grid = (N,)
-    first = 1 + rank * M  # weak scaling: each rank its own replication ids
-    theta = torch.empty((M, 1), dtype=torch.float64, device="cuda")
-    gathered = [torch.empty((M, 1), dtype=torch.float64, device=coll_dev) for _ in range(world)]
+    # strong scaling: the fixed M split over the ranks (harness.py:349-358)
+    counts = [shard(M, world, r)[1] for r in range(world)]
+    off, count = shard(M, world, rank)
+    first = 1 + off
+    width = max(counts)
+    theta = torch.zeros((width, 1), dtype=torch.float64, device="cuda")
+    gathered = [torch.empty((width, 1), dtype=torch.float64, device=coll_dev)
+                for _ in range(world)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def barrier():
@@ -263,17 +297,23 @@ def run_ours(args) -> dict:
         torch.cuda.synchronize()
 
     def one_step():
-        h, n, keep = device_step(gen_id, model, SEED, first, M, grid, theta, lib, C, _lib)
+        h, n = None, 0
+        if count:
+            h, n, _ = device_step(gen_id, model, SEED, first, count, grid, theta, lib, C, _lib)
         if use_dist:  # the one collective: theta of every rank, once per step
             dist.all_gather(gathered, theta if not shared_dev else theta.cpu())
         return h, n
+
+    def release(h):
+        if h is not None:
+            lib.rq_sampler_destroy(h)
 
     peak, peak_ms = _lib.fp64_peak()
     launches = 0
     for _ in range(args.warmup):
         h, _ = one_step()
         torch.cuda.synchronize()
-        lib.rq_sampler_destroy(h)
+        release(h)
     clocks = ClockSampler(local)
     clocks.start()
     step_ms = []
@@ -285,7 +325,7 @@ def run_ours(args) -> dict:
         h, n = one_step()
         b.record()
         b.synchronize()
-        lib.rq_sampler_destroy(h)
+        release(h)
         launches += n
         step_ms.append(a.elapsed_time(b))
     clk = clocks.stop()
@@ -294,18 +334,22 @@ def run_ours(args) -> dict:
     if use_dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    paths = M * N * world
-    value = paths / (ms * 1e-3)
+    value = M * N / (ms * 1e-3)
+    if use_dist:
+        full = np.concatenate([g[:c].cpu().numpy() for g, c in zip(gathered, counts)])
+    else:
+        full = theta[:count].cpu().numpy()
+    theta_sha = hashlib.sha256(np.ascontiguousarray(full, dtype=np.float64).tobytes()).hexdigest()
 
     # kernel share: one extra (untimed) step with per-kernel CUDA events
     _lib.stats_reset(timing=True)
     h, _ = one_step()
     torch.cuda.synchronize()
-    lib.rq_sampler_destroy(h)
+    release(h)
     ks = _lib.stats_get()
     _lib.stats_reset(timing=False)
     W = slots_per_path(model)
-    achieved = M * N * W / (ks["paths_ms"] * 1e-3)  # per GPU, slots/s
+    achieved = count * N * W / max(ks["paths_ms"] * 1e-3, 1e-12)  # this GPU, slots/s
 
     # end to end through the host API: host in, theta to host every step
     e2e_ms = []
@@ -313,14 +357,15 @@ def run_ours(args) -> dict:
     for k in range(max(1, min(args.steps, 3))):
         barrier()
         t0 = time.perf_counter()
-        estimate_replications(gen, model, SEED, first, M, grid)
+        if count:
+            estimate_replications(gen, model, SEED, first, count, grid)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     tr = _lib.stats_get()
     ne = len(e2e_ms)
     e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=coll_dev)
     if use_dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = paths / (float(e2e_t.item()) * 1e-3)
+    e2e_value = M * N / (float(e2e_t.item()) * 1e-3)
 
     out = None
     if rank == 0:
@@ -333,16 +378,18 @@ def run_ours(args) -> dict:
             "warmup": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (seed 20120224, replication ids from 1, packaged 2012-02-24 "
+            "data": "synthetic (seed 20120224, replication ids 1..M, packaged 2012-02-24 "
                     "Treasury curve)",
-            "config": {"workload": desc, "generator": gen, "M_per_gpu": M, "N": N,
-                       "model": kind, "dim": model.dim,
-                       "parallelism": f"replication-sharded x{world} (theta all-gathered once "
-                                      f"per step{(' over gloo, ranks sharing ' + str(ndev) + ' GPU(s)' if shared_dev else ' over NCCL') if use_dist else ''})",
-                       "l2": "flushed between timed steps (256 MiB write)"},
+            "config": cfg,
+            "parallelism": f"replication-sharded x{world}: fixed M={M} split, "
+                           f"{count} replications on rank 0 (theta all-gathered once per step"
+                           + ((" over gloo, ranks sharing " + str(ndev) + " GPU(s))"
+                               if shared_dev else " over NCCL)") if use_dist else ")"),
+            "M_per_rank": counts,
+            "theta_sha16": theta_sha[:16],
             "roofline": {
                 "bound": "fp64",
                 "kernel": "k_paths_* (fused generator + inverse normal + path + payoff)",
@@ -356,7 +403,7 @@ def run_ours(args) -> dict:
                                                            + ks["setup_ms"], 1e-9),
                 "kernel_ms": {"setup": ks["setup_ms"], "paths": ks["paths_ms"],
                               "reduce": ks["reduce_ms"]},
-                "traffic": traffic_per_launch(args.workload, gen, M, N),
+                "traffic": traffic_per_launch(args.workload, gen, count, N),
                 "traffic_source": TRAFFIC_SOURCE,
                 "ncu_fp64_pipe_pct": _profile_entry(args.workload, gen).get("fp64_pipe_pct"),
             },
@@ -367,7 +414,9 @@ def run_ours(args) -> dict:
             "clocks": clk,
         }
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline: N=1 runs only
-            out["cpu_baseline"] = cpu_baseline(model, gen, N, args)
+            cb, par = cpu_baseline(model, gen, M, N, full[:, 0])
+            out["cpu_baseline"] = cb
+            out["parity"] = par
         if args.workload == "c2" and not use_dist and not args.reps:
             out["comparison"] = generator_comparison(model, M, N)
     if use_dist:
@@ -403,30 +452,69 @@ def generator_comparison(model, M: int, N: int) -> dict:
 
 
 # ---------------------------------------------------------------- reference arm
-def cpu_sample(model, gen, N, reps, threads):
+def _sobol_v(model, gen):
+    if not gen.startswith("sobol"):
+        return None
+    from paper_1408_5526_b200.tables import sobol_directions
+
+    return sobol_directions(model.dim)
+
+
+def cpu_theta(model, gen, ids, N, threads):
+    """(theta[ids], seconds): the oracle on replication ids (runs of
+    consecutive ids), `threads` host threads, each owning whole replications
+    (harness.py:349-358)."""
+    import numpy as np
+
     from oracle import oracle as O
 
-    sob = None
-    if gen.startswith("sobol"):
-        from paper_1408_5526_b200.tables import sobol_directions
+    runs = np.split(ids, np.where(np.diff(ids) != 1)[0] + 1)
+    # the runs go concurrently (the ctypes call releases the GIL), the host
+    # threads split in proportion to their replications, so every thread
+    # owns whole replications as in one run
+    share = [max(1, round(threads * len(r) / len(ids))) for r in runs]
+    th = [None] * len(runs)
+    sob = _sobol_v(model, gen)
 
-        sob = sobol_directions(model.dim)
+    def go(k):
+        r = runs[k]
+        th[k] = O.run_replications(gen, model, SEED, int(r[0]), len(r), (N,), threads=share[k],
+                                   sobol_v=sob)[:, 0]
+
     t0 = time.perf_counter()
-    O.run_replications(gen, model, SEED, 1, reps, (N,), threads=threads, sobol_v=sob)
-    return reps * N / (time.perf_counter() - t0)
+    pool = [threading.Thread(target=go, args=(k,)) for k in range(len(runs))]
+    for t in pool:
+        t.start()
+    for t in pool:
+        t.join()
+    return np.concatenate(th), time.perf_counter() - t0
 
 
-def cpu_baseline(model, gen, N, args) -> dict:
+THETA_RTOL = 1e-12  # north_star: per-replication estimates within ~1e-12 (FP64)
+
+
+def cpu_baseline(model, gen, M, N, theta_gpu) -> tuple[dict, dict]:
+    """The oracle on `cores` replications at full N -- the first and the last
+    ids of 1..M -- timed on the host cores, and their theta against the
+    GPU's (theta_gpu[m - 1] for id m)."""
+    import numpy as np
+
     from oracle import oracle as O
 
     cores = O.host_cores()
-    reps = max(2, cores) if model.name == "libor" and model.dim <= 20 else max(2, cores // 2)
-    n = N if model.dim <= 20 else max(8192, N // 16)
-    rate = cpu_sample(model, gen, n, reps, cores)
-    return {"value": rate, "unit": "paths/s", "cores": cores, "kind": "port",
-            "sample": f"{reps} replications x N={n} of the same workload ({gen}), "
-                      f"oracle/rqmc_oracle.c (bit-exact C restatement of the reference numba "
-                      f"path), {cores} threads"}
+    ids = parity_ids(M, cores)
+    ref, sec = cpu_theta(model, gen, ids, N, cores)
+    got = theta_gpu[ids - 1]
+    rel = float(np.max(np.abs(got / ref - 1.0)))
+    span = f"{ids[0]}-{ids[(len(ids) + 1) // 2 - 1]},{ids[(len(ids) + 1) // 2]}-{ids[-1]}" \
+        if len(ids) > 1 else str(ids[0])
+    cb = {"value": len(ids) * N / sec, "unit": "paths/s", "cores": cores, "kind": "port",
+          "sample": f"{len(ids)} replications (ids {span}) x N={N} of the same workload "
+                    f"({gen}), oracle/rqmc_oracle.c (bit-exact C restatement of the "
+                    f"reference numba path), {cores} threads"}
+    par = {"reps": int(len(ids)), "ids": span, "max_rel_err": rel, "tol": THETA_RTOL,
+           "ok": bool(rel <= THETA_RTOL), "bit_exact_reps": int(np.sum(got == ref))}
+    return cb, par
 
 
 def run_reference(args) -> dict | None:
@@ -435,16 +523,24 @@ def run_reference(args) -> dict | None:
         return None
     from oracle import oracle as O
 
-    kind, mat, acc, M, N, desc = WORKLOADS[args.workload]
-    model = build_model(kind, mat, acc)
+    model, M, N, desc, cfg = workload_config(args)
+    gen = args.generator
     cores = O.host_cores()
-    reps = max(2, cores)
+    # bounded per-step sample: `cores` whole replications (C2: full N; the
+    # long-path workloads at N/16 -- paths/s is independent of N)
     n = N if model.dim <= 20 else max(8192, N // 16)
+    ids = parity_ids(M, cores)
     for _ in range(args.warmup):
-        cpu_sample(model, args.generator, 8192, 2, cores)
-    rates = [cpu_sample(model, args.generator, n, reps, cores) for _ in range(args.steps)]
+        cpu_theta(model, gen, ids[:2], 8192, cores)
+    rates = []
+    for _ in range(args.steps):
+        _, sec = cpu_theta(model, gen, ids, n, cores)
+        rates.append(len(ids) * n / sec)
     v = float(statistics.median(rates))
-    samp = f"{reps} replications x N={n} per step, {args.generator}"
+    _, sec1 = cpu_theta(model, gen, ids[:1], n, 1)  # workers = 1
+    samp = (f"{len(ids)} replications x N={n} per step (of M={M} x N={N}), {gen}, "
+            f"{cores} threads (oracle/rqmc_oracle.c, bit-exact restatement of the reference "
+            f"numba kernels)")
     return {
         "metric": "RQMC paths/sec (LIBOR caplet, MBS) at 1/2/4/8 B200; % FP64 pipe peak",
         "impl": "reference",
@@ -453,16 +549,18 @@ def run_reference(args) -> dict | None:
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": reps * n / v * 1e3,
+        "ms_per_step": len(ids) * n / v * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seed 20120224)",
-        "config": {"workload": desc, "generator": args.generator, "M": M, "N": N},
+        "data": "synthetic (seed 20120224, replication ids 1..M, packaged 2012-02-24 "
+                "Treasury curve)",
+        "config": cfg,
         "cpu_baseline": {"value": v, "unit": "paths/s", "cores": cores, "kind": "port",
-                         "sample": samp + " (oracle/rqmc_oracle.c, bit-exact restatement of "
-                                          "the reference numba kernels)"},
+                         "sample": samp},
+        "workers_1": {"value": n / sec1, "unit": "paths/s", "cores": 1,
+                      "sample": f"1 replication x N={n}, 1 thread"},
         "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -49,15 +49,25 @@ enum rq_generator {
 
 /* Model kinds: models.LiborModel (models.py:296-329), models.MbsModel
  * (models.py:452-469), models.FirstCoordinateModel / ConstantModel
- * (models.py:477-498). */
-enum rq_model_kind { RQ_MODEL_LIBOR = 0, RQ_MODEL_MBS = 1, RQ_MODEL_X1 = 2, RQ_MODEL_CONST1 = 3 };
+ * (models.py:477-498).  RQ_MODEL_XHASH is a test integrand with no
+ * reference counterpart: payoff = top 20 bits of a 64-bit hash of every
+ * coordinate's bit pattern in dimension order (h = 0x6A09E667F3BCC909;
+ * per coordinate h = (h ^ bits(u)) * 0x9E3779B97F4A7C15, h ^= h >> 32),
+ * so an exact theta pins all coordinates of all paths. */
+enum rq_model_kind {
+  RQ_MODEL_LIBOR = 0,
+  RQ_MODEL_MBS = 1,
+  RQ_MODEL_X1 = 2,
+  RQ_MODEL_CONST1 = 3,
+  RQ_MODEL_XHASH = 5
+};
 
 /* Model description = the arguments of the reference's payoff kernels
  * (_libor_payoffs models.py:271, _mbs_payoffs models.py:430).
  * LIBOR: dim = steps (10, 20, 40 or 80), delta = accrual, sigma, strike,
  *        front_factor = 1/(1 + delta*L_0(0)), table = l0[dim] (HOST).
  * MBS:   dim = months, i0..payment as MbsConfig, table = ck[dim] (HOST).
- * X1 / CONST1: dim only. */
+ * X1 / CONST1 / XHASH: dim only. */
 typedef struct rq_model {
   int32_t kind;
   int32_t dim;

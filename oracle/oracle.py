@@ -22,7 +22,7 @@ LIB_PATH = HERE / "build" / "librqmc_oracle.so"
 GEN_IDS = {"rasrap-recursive": 0, "rasrap-counter": 1, "philox": 2, "sobol-gray": 3,
            "sobol-counter": 4, "sfc64": 5, "twister": 6, "xorwow": 7,
            "kakutani": 8}
-MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3}
+MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3, "xhash": 5}
 FAMILY_IDS = {"twister": 1, "xorwow": 2, "philox": 3, "rasrap": 4, "sobol": 5, "kakutani": 6,
               "sfc64": 7}
 
@@ -75,6 +75,8 @@ def _declare(L):
     L.orc_inv_normal_n.argtypes = [P(dbl), i64, P(dbl)]
     L.orc_libor_payoffs.argtypes = [P(dbl), i64, i32, P(dbl), dbl, dbl, dbl, dbl, P(dbl)]
     L.orc_mbs_payoffs.argtypes = [P(dbl), i64, i32] + [dbl] * 8 + [P(dbl), P(dbl)]
+    L.orc_coord_hash.restype = dbl
+    L.orc_coord_hash.argtypes = [P(dbl), i32]
     L.orc_pairwise_sum.restype = dbl
     L.orc_pairwise_sum.argtypes = [P(dbl), i64]
     L.orc_run_replication.argtypes = [i32, i32, i32, P(dbl), u64, i64, P(i64), i32,
@@ -290,6 +292,12 @@ def mbs_payoffs(u, i0, k0, k1, k2, k3, k4, sigma_xi, payment, ck) -> np.ndarray:
     lib().orc_mbs_payoffs(_p(u, C.c_double), u.shape[0], u.shape[1], i0, k0, k1, k2, k3, k4,
                           sigma_xi, payment, _p(ck, C.c_double), _p(out, C.c_double))
     return out
+
+
+def coord_hash(u) -> np.ndarray:
+    """xhash test-integrand payoffs of uniforms u[n, dim] (rqmc_oracle.c)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    return np.array([lib().orc_coord_hash(_p(r, C.c_double), u.shape[1]) for r in u])
 
 
 def pairwise_sum(a) -> float:

@@ -815,6 +815,21 @@ int orc_kakutani_points(int dim, uint64_t key, int64_t count, double *out) {
 
 #define CHUNK_PATHS 8192 /* harness.py:25 */
 
+/* Test integrand with no reference counterpart (RQ_MODEL_XHASH,
+ * include/rqmc_b200.h): top 20 bits of a 64-bit hash of the coordinates'
+ * bit patterns in dimension order.  Exact sums, so theta pins every
+ * coordinate of every path of the device stream. */
+double orc_coord_hash(const double *u, int dim) {
+  uint64_t h = 0x6A09E667F3BCC909ull;
+  for (int d = 0; d < dim; d++) {
+    uint64_t b;
+    memcpy(&b, &u[d], 8);
+    h = (h ^ b) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 32;
+  }
+  return (double)(h >> 44);
+}
+
 /* seeding.py:17-24 (twister 1, xorwow 2, philox 3, rasrap 4, sobol 5, kakutani 6);
  * 7 = sfc64 */
 static const uint64_t FAMILY_ID[9] = {4, 4, 3, 5, 5, 7, 1, 2, 6};
@@ -822,7 +837,7 @@ static const uint64_t FAMILY_ID[9] = {4, 4, 3, 5, 5, 7, 1, 2, 6};
 int orc_run_replication(int gen, int model, int dim, const double *mparams, uint64_t seed,
                         int64_t m, const int64_t *grid, int ngrid, const uint32_t *sobol_v,
                         double *theta) {
-  if (gen < 0 || gen > 8 || model < 0 || model > 3 || ngrid < 1) return -1;
+  if (gen < 0 || gen > 8 || model < 0 || model > 5 || model == 4 || ngrid < 1) return -1;
   int64_t nmax = grid[ngrid - 1];
   uint64_t parts[3] = {seed, FAMILY_ID[gen], (uint64_t)m};
   uint64_t key = orc_derive_key(parts, 3); /* harness.py:113 */
@@ -885,6 +900,8 @@ int orc_run_replication(int gen, int model, int dim, const double *mparams, uint
                       mparams[4], mparams[5], mparams[6], mparams[7], mparams + 8, out);
     } else if (model == 2) {
       for (int64_t i = 0; i < cnt; i++) out[i] = buf[i * dim];
+    } else if (model == 5) {
+      for (int64_t i = 0; i < cnt; i++) out[i] = orc_coord_hash(buf + i * dim, dim);
     } else {
       for (int64_t i = 0; i < cnt; i++) out[i] = 1.0;
     }

@@ -83,6 +83,7 @@ void orc_mbs_payoffs(const double *u, int64_t npaths, int months, double i0, dou
 
 /* numpy pairwise sum of a contiguous float64 vector (np.sum) */
 double orc_pairwise_sum(const double *a, int64_t n);
+double orc_coord_hash(const double *u, int dim); /* xhash test integrand (no reference counterpart) */
 
 /* One full replication (harness.py:291-315): generator -> model -> prefix
  * estimates theta[g] = np.sum(payoffs[:grid[g]]) / grid[g].

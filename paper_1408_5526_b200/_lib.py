@@ -31,7 +31,7 @@ GEN_IDS = {
     "xorwow": 7,
     "kakutani": 8,
 }
-MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3}
+MODEL_IDS = {"libor": 0, "mbs": 1, "x1": 2, "const1": 3, "xhash": 5}
 
 # kernels each ABI call launches when it succeeds are counted by the library
 # itself (rq_estimate / rq_run_replications kernel_launches argument).

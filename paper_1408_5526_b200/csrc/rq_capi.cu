@@ -783,7 +783,8 @@ int rq_sampler_rasrap_tables(rq_sampler *s, int32_t rep_local, uint16_t *digits_
 static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, double **tab_dev,
                            cudaStream_t s) {
   if (!m) return fail(RQ_ERR_VALUE, "model is NULL");
-  if (m->kind < 0 || m->kind > rq::MODEL_CONST1) return fail(RQ_ERR_VALUE, "unknown model kind %d", m->kind);
+  if (m->kind < 0 || m->kind == rq::MODEL_POINTS || m->kind > rq::MODEL_XHASH)
+    return fail(RQ_ERR_VALUE, "unknown model kind %d", m->kind);
   if (m->dim != dim) return fail(RQ_ERR_VALUE, "model dim %d != sampler dim %d", m->dim, dim);
   if (m->kind == rq::MODEL_LIBOR && (m->dim < 1 || m->dim > rq::LIBOR_DYN_MAX))
     return fail(RQ_ERR_VALUE, "LIBOR steps %d outside 1..%d", m->dim, rq::LIBOR_DYN_MAX);

@@ -38,6 +38,7 @@ enum ModelKind : int {
   MODEL_X1 = 2,
   MODEL_CONST1 = 3,
   MODEL_POINTS = 4,  // internal: write the uniforms (sampler.fill of a sequential stream)
+  MODEL_XHASH = 5,   // test integrand: hash of every coordinate's bits (rq_kernels.cu ModelHash)
 };
 
 // Per-dimension Halton constants (depend only on the d-th prime).  Offsets

@@ -1928,6 +1928,7 @@ struct ModelMbs {
         N = fma(N, u[m], R * fma(w[m], __ldg(ck + d0 + kk + m), omw));
       }
       rate = r;
+      rescale();
     }
     for (; kk < Dc; kk++) {
       const double u = 1.0 + rate;
@@ -1937,6 +1938,19 @@ struct ModelMbs {
       const double w = fma(k2, atan_mbs(fma(k3, rate, k4)), k1);
       omw = 1.0 - w;
       N = fma(N, u, R * fma(w, __ldg(ck + d0 + kk), omw));
+    }
+    rescale();
+  }
+  // P = prod (1 + i) overflows for high-variance rates (the reference's
+  // disc = 1/P underflows harmlessly instead): once P passes 2^512, scale
+  // P, N and the undiscounted cash-flow factor R together by 2^-512 -- exact
+  // (N_k = sum_j a_j P_k / P_j keeps its value over P), and the later cash
+  // flows carry the same factor.  One integer compare per group of months.
+  __device__ __forceinline__ void rescale() {
+    if (__double2hiint(P) >= 0x5FF00000) {
+      P *= 0x1p-512;
+      N *= 0x1p-512;
+      R *= 0x1p-512;
     }
   }
   __device__ double payoff() const { return N / P; }
@@ -1957,6 +1971,33 @@ struct ModelTest {
     if (!CONST1 && Dc > 0) f = zcol[0];
   }
   __device__ double payoff() const { return f; }
+};
+
+// Test integrand with no reference counterpart: a 64-bit hash of the bit
+// patterns of ALL coordinates in dimension order, payoff = its top 20 bits
+// as a double.  Sums of such payoffs are exact (< 2^53), so theta pins every
+// coordinate of every path bit for bit through the production path kernel
+// (the x1 integrand only sees dimension 0).  Oracle: rqmc_oracle.c
+// coord_hash (same constants).
+constexpr uint64_t XHASH_INIT = 0x6A09E667F3BCC909ull;
+constexpr uint64_t XHASH_MUL = 0x9E3779B97F4A7C15ull;
+__device__ __forceinline__ uint64_t xhash_step(uint64_t h, double u) {
+  h = (h ^ (uint64_t)__double_as_longlong(u)) * XHASH_MUL;
+  return h ^ (h >> 32);
+}
+struct ModelHash {
+  static constexpr bool NORMALS = false;
+  static constexpr bool SMALL_LIBOR = false;
+  static constexpr int MINB = 4;
+  using Shared = NoShared;
+  static __host__ __device__ int gen_dims(int dim) { return dim; }
+  uint64_t h;
+  __device__ void init(const ModelParams &, Shared &) {}
+  __device__ void begin() { h = XHASH_INIT; }
+  __device__ void chunk(int, int Dc, const double *zcol) {
+    for (int k = 0; k < Dc; k++) h = xhash_step(h, zcol[k * TILE]);
+  }
+  __device__ double payoff() const { return (double)(h >> 44); }
 };
 
 // ======================================================================
@@ -2639,6 +2680,7 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
       return paths_gm<G, ModelMbs>(a, launched, s, probe, blocks);
     case MODEL_X1: return paths_gm<G, ModelTest<false>>(a, launched, s, probe, blocks);
     case MODEL_CONST1: return paths_gm<G, ModelTest<true>>(a, launched, s, probe, blocks);
+    case MODEL_XHASH: return paths_gm<G, ModelHash>(a, launched, s, probe, blocks);
   }
   return cudaErrorInvalidValue;
 }
@@ -2759,6 +2801,7 @@ static cudaError_t seq_g(const PathArgs &a, const SeqArgs &q, int blocks, int *l
       return seq_gm<G, ModelMbs>(a, q, blocks, launched, s, occ);
     case MODEL_X1: return seq_gm<G, ModelTest<false>>(a, q, blocks, launched, s, occ);
     case MODEL_CONST1: return seq_gm<G, ModelTest<true>>(a, q, blocks, launched, s, occ);
+    case MODEL_XHASH: return seq_gm<G, ModelHash>(a, q, blocks, launched, s, occ);
     case MODEL_POINTS: return seq_gm<G, ModelPoints>(a, q, blocks, launched, s, occ);
   }
   return cudaErrorInvalidValue;

@@ -37,6 +37,46 @@ def shard(total: int, world: int, rank: int) -> tuple[int, int]:
     return first, base + (1 if rank < extra else 0)
 
 
+def bind_device() -> None:
+    """Under torchrun, put this rank on GPU LOCAL_RANK (mod the visible GPUs)
+    unless the caller already moved it off device 0."""
+    import os
+
+    import torch
+
+    if "LOCAL_RANK" not in os.environ or not torch.cuda.is_available():
+        return
+    n = torch.cuda.device_count()
+    want = int(os.environ["LOCAL_RANK"]) % max(1, n)
+    if torch.cuda.current_device() == 0 and want != 0:
+        torch.cuda.set_device(want)
+
+
+_ERRORS = {"ArithmeticError": ArithmeticError, "ValueError": ValueError,
+           "RuntimeError": RuntimeError}
+
+
+def _raise_collective(status, group=None) -> None:
+    """Re-raise the first failing rank's error on EVERY rank (same type), so
+    no rank is left blocked in the data gather (the reference raises
+    ArithmeticError cleanly from its one process)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    every = [None] * world
+    dist.all_gather_object(every, status, group=group)
+    for r, st in enumerate(every):
+        if st is None:
+            continue
+        kind, msg = st
+        if kind == "ConfigurationError":
+            from .harness import ConfigurationError
+
+            raise ConfigurationError(f"rank {r}: {msg}")
+        cls = _ERRORS.get(kind, RuntimeError)
+        raise cls(f"rank {r}: {kind}: {msg}" if cls is RuntimeError else f"rank {r}: {msg}")
+
+
 def gather_rows(local: np.ndarray, total: int, group=None) -> np.ndarray:
     """All-gather row blocks of a [count, k] float64 matrix in rank order."""
     import torch
@@ -65,8 +105,13 @@ def estimate_sharded(generator: str, model, seed: int, replications: int, grid,
     est = estimator or estimate_replications
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     first, count = shard(replications, world, rank)
+    if estimator is None:
+        bind_device()
+    local, status = np.zeros((count, len(grid))), None
     if count:
-        local = est(generator, model, seed, 1 + first, count, grid)
-    else:
-        local = np.zeros((0, len(grid)))
+        try:
+            local = np.asarray(est(generator, model, seed, 1 + first, count, grid))
+        except Exception as e:  # noqa: BLE001 -- re-raised on every rank below
+            status = (type(e).__name__, str(e))
+    _raise_collective(status, group)
     return gather_rows(local, replications, group)

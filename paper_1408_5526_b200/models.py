@@ -274,6 +274,31 @@ class FirstCoordinateModel:
         return np.array(u[:, 0], dtype=np.float64, copy=True)
 
 
+class CoordinateHashModel:
+    """Test integrand with no reference counterpart: payoff = the top 20
+    bits of a 64-bit hash of every coordinate's bit pattern, in dimension
+    order (include/rqmc_b200.h RQ_MODEL_XHASH).  Sums of such payoffs are
+    exact, so theta pins all coordinates of all paths bit for bit where
+    x1 only pins dimension 0."""
+
+    name = "xhash"
+    INIT = 0x6A09E667F3BCC909
+    MUL = 0x9E3779B97F4A7C15
+
+    def __init__(self, dim: int = 20):
+        self.dim = dim
+
+    def payoffs(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        bits = u.view(np.uint64)
+        h = np.full(u.shape[0], self.INIT, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            for d in range(u.shape[1]):
+                h = (h ^ bits[:, d]) * np.uint64(self.MUL)
+                h ^= h >> np.uint64(32)
+        return (h >> np.uint64(44)).astype(np.float64)
+
+
 def _payoffs(model, u):
     torch = _lib.require_cuda()
     t, host = _as_device(u)

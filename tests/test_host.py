@@ -190,3 +190,72 @@ def test_gather_over_gloo_is_world_size_invariant(world, total):
     expect = np.array([[1 + r + n * 1e-6 for n in (10, 20)] for r in range(total)])
     for _, theta in res:
         assert np.array_equal(theta, expect)
+
+
+def _failing_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def est(gen, model, seed, first, count, grid):
+        if first > 1:  # only the last rank's shard "produces a NaN"
+            raise ArithmeticError(f"replication {first} produced a non-finite estimate")
+        return np.ones((count, len(grid)))
+
+    try:
+        D.estimate_sharded("philox", None, SEED, 8, (10,), estimator=est)
+        q.put((rank, None))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, (type(e).__name__, str(e))))
+    dist.destroy_process_group()
+
+
+def test_sharded_error_reaches_every_rank():
+    """one rank's ArithmeticError must not leave the others
+    blocked in the gather -- every rank re-raises the same error type."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_failing_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        assert res[r] is not None and res[r][0] == "ArithmeticError", res
+        assert "rank 1" in res[r][1]
+
+
+@pytest.mark.timeout(600)
+def test_sharded_oracle_under_torchrun_matches_one_process(oracle):
+    """Strong-scaling host path under torchrun (2 ranks, gloo, CPU): the
+    fixed M split over ranks, real estimator (the oracle standing in for the
+    device), theta gathered once -- bit-identical to one process."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29541", "tests/_torchrun_sharded.py"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    from paper_1408_5526_b200 import models as M
+
+    model = M.LiborModel(M.LiborConfig(maturity=5.0, accrual=0.25))
+    ref = oracle.run_replications("philox", model, SEED, 1, 7, (1000, 4096), threads=4)
+    assert d["world"] == 2 and d["counts"] == [4, 3]
+    assert np.array_equal(np.array(d["theta"]), ref)

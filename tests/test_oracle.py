@@ -302,3 +302,13 @@ def test_kakutani_estimates_bit_exact(oracle, golden):
         mine = oracle.run_replications("kakutani", models[mk], SEED, 1, theta.shape[1],
                                        g[f"{tag}_grid"], threads=4)
         assert np.array_equal(mine.T, theta), tag
+
+
+def test_xhash_model_definitions_agree(oracle):
+    """The package's host definition of the coordinate hash == the oracle's."""
+    from paper_1408_5526_b200 import models as M
+
+    u = np.random.default_rng(3).random((257, 37))
+    h = M.CoordinateHashModel(37).payoffs(u)
+    assert np.array_equal(h, oracle.coord_hash(u))
+    assert h.min() >= 0 and h.max() < 2**20 and len(np.unique(h)) > 250
