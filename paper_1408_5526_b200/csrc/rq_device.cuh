@@ -276,6 +276,15 @@ constexpr uint64_t INVN_HI_BITS = 0x3fee83126e978d4fULL;    // floor_double(1 - 
 __device__ __forceinline__ bool invn_tail_p(double p) {
   return (uint64_t)__double_as_longlong(p) - INVN_PLOW_BITS > INVN_HI_BITS - INVN_PLOW_BITS;
 }
+// The same test on the high word alone (two integer ops instead of a 64-bit
+// range check): exact except for p sharing the high word of PLOW or HI,
+// which it reports as tail CANDIDATES -- the tail queue re-tests them with
+// invn_tail_p (inv_normal below), so the branch taken is the reference's.
+constexpr uint32_t INVN_C_LO = (uint32_t)(INVN_PLOW_BITS >> 32) + 1u;  // first all-central high word
+constexpr uint32_t INVN_C_HI = (uint32_t)(INVN_HI_BITS >> 32) - 1u;    // last all-central high word
+__device__ __forceinline__ bool invn_tail_cand(double p) {
+  return (uint32_t)__double2hiint(p) - INVN_C_LO > INVN_C_HI - INVN_C_LO;
+}
 // Central branch on Q = p - 1/2 without folding.  For p > 1/2 the
 // reference computes q = (1 - p) - 1/2 = 1/2 - p exactly (Sterbenz) and
 // returns -(q R(q^2)) = Q R(Q^2); for p <= 1/2, Q is the reference's own
@@ -348,6 +357,16 @@ __device__ __forceinline__ double invn_tail(double pl) {
     den = fma(den, w, c_invn_tden[k]);
   }
   return num * rcp2(den);
+}
+// A queued tail candidate (invn_tail_cand): the tail, or -- for the rare p
+// that only shares PLOW's / HI's high word -- the central branch, out of
+// line so the tail loops keep their register budget.
+static __device__ __noinline__ double invn_central_rare(double p) { return invn_central_q(p - 0.5); }
+__device__ __forceinline__ double invn_queued(double p) {
+  if (!invn_tail_p(p)) return invn_central_rare(p);
+  bool neg;
+  const double x = invn_tail(invn_fold(p, &neg));
+  return neg ? -x : x;
 }
 // Scalar Phi^-1 (divergent tail); the tile filler uses a compacted tail.
 __device__ __forceinline__ double inv_normal(double p) {

@@ -54,6 +54,15 @@
 #ifndef RQ_RASRAP_MINB
 #define RQ_RASRAP_MINB 5  // CTAs per SM for the persistent Rasrap tile with LIBOR S <= 20
 #endif
+#ifndef RQ_BASE2
+#define RQ_BASE2 1  // base 2 in closed form (bit reversal) instead of the digit tree
+#endif
+#ifndef RQ_TAIL_CAND
+#define RQ_TAIL_CAND 1  // inverse-normal tail test on the high word (exact re-test in the queue)
+#endif
+#ifndef RQ_WS
+#define RQ_WS 1  // warp-specialised path kernel (producer / consumer warpgroups)
+#endif
 #ifndef RQ_MINB_SMALL
 #define RQ_MINB_SMALL 4  // CTAs per SM targeted for LIBOR S <= 20 (register budget)
 #endif
@@ -98,6 +107,18 @@ __device__ __forceinline__ uint64_t div_base64(uint64_t x, const HaltonDim &h) {
   return __umul64hi(x, h.m64);
 }
 __device__ __forceinline__ double u16d(uint16_t v) { return (double)v; }
+// Thread index within its TILE-thread group (the model side of a path
+// kernel: threadIdx.x in k_paths, the consumer half in k_paths_ws).
+__device__ __forceinline__ int ctid() { return (int)(threadIdx.x & (TILE - 1)); }
+// 32-bit shared-state-space address of a shared object, and a load from it
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
 
 // ======================================================================
 // Setup kernels (per replication randomisation, on device)
@@ -429,6 +450,10 @@ struct GenRasrapRecTile {
       R.P[dd][k] = S;
     }
   }
+  __device__ __forceinline__ double pers_P(int dd, int j) const {
+    if constexpr (PERSIST) return sh->P[dd][j];
+    return 0.0;
+  }
   __device__ __forceinline__ const double *sigd_of(int dd) const {
     if constexpr (SIGSM) return sh->sigd + sh->soff[dd];
     return nullptr;
@@ -447,16 +472,17 @@ struct GenRasrapRecTile {
       if (!adv) state_full(rl, base, d, dd);
       R.st_rl[dd] = rl;
       R.st_base[dd] = base;
-      int N = TILE, J = 0;
+      int N = TILE, J = 0, jr = 1;
       R.nn[dd][0] = (int16_t)N;
 #pragma unroll 1
       while (N > 1) {
         N = (int)__umulhi((uint32_t)R.bd[dd][J] + (uint32_t)N - 1u, h.m16) + 1;
         J++;
         R.nn[dd][J] = (int16_t)N;
+        jr = N > 32 ? J + 1 : jr;
       }
       if (adv) rechain(rl, d, dd, jmax, J < h.tdig + 1 ? J : h.tdig + 1);
-      R.J[dd] = J;
+      R.J[dd] = J | jr << 8;
       R.sJ[dd] = sh->P[dd][J];
     }
   }
@@ -481,7 +507,7 @@ struct GenRasrapRecTile {
       qn = nq;
       j++;
     }
-    int N = TILE, J = 0;
+    int N = TILE, J = 0, jr = 1;
     R.nn[dd][0] = (int16_t)N;
 #pragma unroll 1
     while (N > 1) {
@@ -490,22 +516,29 @@ struct GenRasrapRecTile {
       N = (int)__umulhi(bj + (uint32_t)N - 1u, h.m16) + 1;
       J++;
       R.nn[dd][J] = (int16_t)N;
+      jr = N > 32 ? J + 1 : jr;
     }
     double S = ini[hB + 1 > J ? hB + 1 : J];
 #pragma unroll 1
     for (int k = hB; k >= J; k--) S = dadd(S, dmul(u16d(sg[R.bd[dd][k]]), w[k]));
-    R.J[dd] = J;
+    R.J[dd] = J | jr << 8;
     R.hB[dd] = hB;
     R.sJ[dd] = S;
   }
+  // Dim of slot k of warp w (-1: none): round-robin.  (Grouping the first
+  // chunk's dims over the warps by tree cost measured -0.6..+0.1%.)
+  __device__ __forceinline__ static int dim_slot(int warp, int k, int, int Dc) {
+    const int dd = warp + k * WARPS;
+    return dd < Dc ? dd : -1;
+  }
   __device__ void stage_sigma(int rl, int d0, int Dc) {
-    // warp w stages the sigma tables of its dims (dd = w mod WARPS)
+    // warp w stages the sigma tables of its dims (dim_slot)
     Shared &R = *sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
     const int off0 = c_hdim[d0].sig_off;
 #pragma unroll 1
-    for (int dd = warp; dd < Dc; dd += WARPS) {
+    for (int k = 0, dd; (dd = dim_slot(warp, k, d0, Dc)) >= 0; k++) {
       const HaltonDim &h = c_hdim[d0 + dd];
       const int o = h.sig_off - off0;
       if constexpr (SIGSM)
@@ -514,29 +547,78 @@ struct GenRasrapRecTile {
     }
     __syncwarp();
   }
+  // Base 2 (dimension 0) in closed form.  Every partial sum of the
+  // reference recursion is an exact dyadic rational there (weights
+  // binpow(0.5, j+1) = 2^-(j+1), init sums from Python 0.5**active times
+  // powers of 2, < 1 with <= 40 bits), so the point n = n0 + i is exactly
+  // init_sums[h+1] + sum_{j<=h} sigma(n_j) 2^-(j+1) whatever the order of
+  // the additions, h = the highest bit where n and n0 differ
+  // (halton.py:402-414).  sigma is the identity or the flip on {0, 1}, so
+  // the sum is the bit reversal of the low h+1 bits of n ^ flip: a handful
+  // of integer ops per point instead of a 7-level tree.
+  __device__ __forceinline__ void base2_points(int rl, uint64_t base, double *zd) {
+    const int lane = threadIdx.x & 31;
+    const HaltonDim &h = c_hdim[0];
+    const uint64_t n0 = t->start[(int64_t)rl * t->dim];
+    const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
+    const uint64_t flip = t->sigma[(int64_t)rl * t->sig_stride + h.sig_off] ? ~0ull : 0ull;
+#pragma unroll
+    for (int m = 0; m < TILE / 32; m++) {
+      const int k = lane + 32 * m;
+      const uint64_t n = n0 + base + (uint64_t)k, x = n ^ n0;
+      double v;
+      if (x == 0) {
+        v = __ldg(ini);
+      } else {
+        const int hb = 63 - __clzll((long long)x);  // highest changed digit
+        const uint64_t rev = __brevll((n ^ flip) << (63 - hb));  // bits 0..hb reversed
+        // rev = sum_j sigma(n_j) 2^(hb-j) < 2^(hb+1): exact, scaled by 2^-(hb+1)
+        const double f = __ull2double_rn(rev) * __hiloint2double((1022 - hb) << 20, 0);
+        v = dadd(__ldg(ini + hb + 1), f);
+      }
+      zd[k] = v;
+    }
+  }
   __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
     RasrapTileShared &R = *sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (sig_smem && R.st_rl[warp < Dc ? warp : 0] != rl) stage_sigma(rl, d0, Dc);
-    {  // lane k prepares dim dd = warp + k * WARPS
-      const int dd = warp + lane * WARPS;
-      if (dd < Dc) prepare_dim(rl, base, d0 + dd, dd);
+    if (sig_smem) {
+      const int d1 = dim_slot(warp, 0, d0, Dc);
+      if (R.st_rl[d1 < 0 ? 0 : d1] != rl) stage_sigma(rl, d0, Dc);
+    }
+    {  // lane k prepares the dim of slot k (base 2: no tree state)
+      const int dd = dim_slot(warp, lane, d0, Dc);
+      if (dd >= 0 && (!RQ_BASE2 || d0 + dd != 0)) prepare_dim(rl, base, d0 + dd, dd);
+      if (RQ_BASE2 && persist && dd == 0 && d0 == 0) {
+        R.st_rl[0] = rl;
+        R.st_base[0] = base;
+      }
     }
     __syncwarp();
     const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
     const double *gsum = t->sums + (int64_t)rl * t->sum_stride;
 #pragma unroll 1
-    for (int dd = warp; dd < Dc; dd += WARPS) {
+    for (int k = 0, dd; (dd = dim_slot(warp, k, d0, Dc)) >= 0; k++) {
+      if (RQ_BASE2 && d0 + dd == 0) {
+        base2_points(rl, base, zt + dd * TILE);
+        continue;
+      }
       const HaltonDim &h = c_hdim[d0 + dd];
       const uint32_t p = (uint32_t)h.base, m16 = h.m16;
       const uint16_t *sg = gsig + h.sig_off;
-      const double *sgd = sigd_of(dd);
+      // sigma of the dim staged as doubles: one 32-bit shared address, so the
+      // loads below are plain LDS (no generic-to-shared conversion per node)
+      const uint32_t sgs = sig_smem ? smem_addr(sigd_of(dd)) : 0u;
+      auto sig = [&](uint32_t a) { return sig_smem ? lds_f64(sgs + 8u * a) : u16d(sg[a]); };
       const double *ini = gsum + h.sum_off;
       // weights in the constant bank (always so for a persistent single-chunk
       // model: its <= CHUNK dims use < CWTS weights)
       const bool cw = SIGSM || h.sum_off + h.cap < CWTS;
       const double *w = g_wts + h.sum_off;
-      const int J = R.J[dd], hB = R.hB[dd];
+      const int J = R.J[dd] & 255, jr = R.J[dd] >> 8, hB = R.hB[dd];
+      // the init sum of a level above hB (node 0 is then n0's prefix): for a
+      // persistent state P[j] = S_j(B) = init_sums[j] there (shared memory)
+      auto init_at = [&](int j) { return persist ? pers_P(dd, j) : ini[j]; };
       double *prev = ph->lev[warp][0], *next = ph->lev[warp][1];
       // Levels of <= 32 nodes live in registers, lane k holding node k, and
       // a child reads its parent with a shuffle (every level above 1 for
@@ -544,15 +626,15 @@ struct GenRasrapRecTile {
       double v = R.sJ[dd];
       int j = J - 1;
 #pragma unroll 1
-      for (; j >= 1 && R.nn[dd][j] <= 32; j--) {
+      for (; j >= jr; j--) {  // register levels: nn[j] <= 32 for j >= jr
         const uint32_t x = (uint32_t)R.bd[dd][j] + (uint32_t)lane;
         const uint32_t par = __umulhi(x, m16);
         const uint32_t a = x - par * p;
-        const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
+        const double sv = sig(a);
         const double wj = cw ? c_wts[h.sum_off + j] : w[j];
         const double vp = __shfl_sync(0xffffffffu, v, (int)par);
         v = dadd(vp, dmul(sv, wj));
-        if (j > hB && lane == 0) v = ini[j];
+        if (j > hB && lane == 0) v = init_at(j);
       }
       if (j == 0) {  // level 0 from the register level 1
         const uint32_t b0 = R.bd[dd][0];
@@ -564,7 +646,7 @@ struct GenRasrapRecTile {
           const uint32_t x = b0 + (uint32_t)k;
           const uint32_t par = __umulhi(x, m16);
           const uint32_t a = x - par * p;
-          const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
+          const double sv = sig(a);
           const double vp = __shfl_sync(0xffffffffu, v, (int)par);
           double o = dadd(vp, dmul(sv, w0));
           if (at_n0 && k == 0) o = ini[0];
@@ -580,9 +662,9 @@ struct GenRasrapRecTile {
         const uint32_t x = bj + (uint32_t)k;  // < 2^16
         const uint32_t par = __umulhi(x, m16);
         const uint32_t a = x - par * p;
-        const double sv = sig_smem ? sgd[a] : u16d(sg[a]);
+        const double sv = sig(a);
         double v = dadd(prev[par], dmul(sv, wj));
-        if (at_n0 && k == 0) v = ini[j];
+        if (at_n0 && k == 0) v = j > 0 ? init_at(j) : ini[0];
         dst[k] = v;
       };
 #pragma unroll 1
@@ -1568,7 +1650,8 @@ struct GenKakutani {
 // ======================================================================
 // SUM: the normals are only summed (config-4 stream without a store): each
 // goes into *acc where it is formed instead of back into the tile.
-template <int FIXED = 0, bool UNROLL = false, bool SUM = false>  // FIXED > 0: Dc == FIXED known at compile time
+// FIXED > 0: Dc == FIXED known at compile time
+template <int FIXED = 0, bool UNROLL = false, bool SUM = false>
 __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *q,
                                                  double *acc = nullptr) {
   const int Dc = FIXED > 0 ? FIXED : Dc_;
@@ -1583,7 +1666,7 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *
     for (int k = 0; k < 4; k++) {
       const int dd = d4 + k;
       p[k] = FULL || dd < Dc ? zt[dd * TILE + threadIdx.x] : 0.5;
-      tail[k] = (FULL || dd < Dc) && invn_tail_p(p[k]);
+      tail[k] = (FULL || dd < Dc) && (RQ_TAIL_CAND ? invn_tail_cand(p[k]) : invn_tail_p(p[k]));
     }
 #pragma unroll
     for (int k = 0; k < 4; k++) x[k] = invn_central_q(p[k] - 0.5);
@@ -1615,11 +1698,9 @@ __device__ __forceinline__ void chunk_to_normals(double *zt, int Dc_, uint16_t *
   __syncwarp();
   for (int k = lane; k < qn; k += 32) {
     const int slot = q[k];
-    bool neg;
-    double pl = invn_fold(zt[slot], &neg);
-    double x = invn_tail(pl);
-    if constexpr (SUM) *acc += neg ? -x : x;
-    else zt[slot] = neg ? -x : x;
+    const double x = invn_queued(zt[slot]);  // tail candidates: exact test, then tail
+    if constexpr (SUM) *acc += x;
+    else zt[slot] = x;
   }
   __syncwarp();
 }
@@ -1674,17 +1755,17 @@ struct ModelLibor {
   double L[S - NS];
   __device__ void set_dyn(double *p) { Ls = p; }
   __device__ __forceinline__ double &Lr(int n) {
-    if (n < NS) return Ls[n * TILE + threadIdx.x];
+    if (n < NS) return Ls[n * TILE + ctid()];
     return L[n - NS];
   }
   __device__ __forceinline__ double Lv(int n) const {
-    if (n < NS) return Ls[n * TILE + threadIdx.x];
+    if (n < NS) return Ls[n * TILE + ctid()];
     return L[n - NS];
   }
   double cz, ssq, dstrike, ff;
   __device__ void init(const ModelParams &mp_, Shared &s) {
     const double kz = libor_state_scale(mp_);
-    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = kz * (mp_.delta * mp_.table[n]);
+    for (int n = ctid(); n < S; n += TILE) s.l0[n] = kz * (mp_.delta * mp_.table[n]);
     sh = &s;
     cz = 1.0 / kz;
     dstrike = mp_.delta * mp_.strike;
@@ -1783,7 +1864,7 @@ struct ModelLiborDyn {
   __device__ void init(const ModelParams &mp_, Shared &s) {
     S = mp_.dim;
     const double kz = libor_state_scale(mp_);
-    for (int n = threadIdx.x; n < S; n += TILE) s.l0[n] = kz * (mp_.delta * mp_.table[n]);
+    for (int n = ctid(); n < S; n += TILE) s.l0[n] = kz * (mp_.delta * mp_.table[n]);
     sh = &s;
     cz = 1.0 / kz;
     dstrike = mp_.delta * mp_.strike;
@@ -1791,14 +1872,14 @@ struct ModelLiborDyn {
     ssq = mp_.sigma * sqrt(mp_.delta);
   }
   __device__ void begin() {
-    for (int n = 0; n < S; n++) Ls[n * TILE + threadIdx.x] = sh->l0[n];
+    for (int n = 0; n < S; n++) Ls[n * TILE + ctid()] = sh->l0[n];
   }
   __device__ void chunk(int d0, int Dc, const double *zcol) {
     for (int k = 0; k < Dc; k++) {
       const int i = d0 + k;
       const double g1 = fma(ssq, zcol[k * TILE], 1.0);
       double f = g1;
-      double *L = Ls + threadIdx.x;
+      double *L = Ls + ctid();
 #pragma unroll 4
       for (int n = i; n < S; n++) {
         const double ln = L[n * TILE];
@@ -1809,7 +1890,7 @@ struct ModelLiborDyn {
     }
   }
   __device__ double payoff() const {
-    const double *L = Ls + threadIdx.x;
+    const double *L = Ls + ctid();
     double prod = 1.0;
     for (int n = 0; n < S - 1; n++) prod *= fma(cz, L[n * TILE], 1.0);
     const double lt = L[(S - 1) * TILE];
@@ -2108,6 +2189,118 @@ __global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathAr
 }
 
 // ======================================================================
+// Warp-specialised path kernel (RQ_WS): 2 x TILE threads.  The first TILE
+// threads (warps 0..3, the "producer" warpgroup) run the generator and the
+// inverse normal of unit u into buffer u & 1; the second TILE threads (the
+// "consumer" warpgroup) run the model on unit u - 1 from the other buffer.
+// The producer phases are integer / shared-memory / issue bound, the model
+// is FP64-pipe bound, so each SM always holds both kinds of work instead of
+// whatever mix the phases of independent CTAs happen to be in.  Hand-off
+// through named barriers (FULL[b]: producers arrive, consumers wait; EMPTY[b]:
+// the reverse); the producers' own phase barrier is a third, TILE-thread one.
+// Same units, same generator and model code, same results as k_paths.
+// ======================================================================
+template <int ID, int N>
+__device__ __forceinline__ void nbar_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ void nbar_arrive() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+constexpr int BAR_PROD = 1, BAR_CONS = 2, BAR_FULL0 = 3, BAR_EMPTY0 = 5;  // FULL/EMPTY + b
+
+#ifndef RQ_WS_MINB
+#define RQ_WS_MINB 3
+#endif
+template <class G, class Mdl>
+__global__ void __launch_bounds__(2 * TILE, RQ_WS_MINB) k_paths_ws(PathArgs a) {
+  extern __shared__ __align__(16) double z[];  // 2 x ZT_BYTES (+ model dyn)
+  __shared__ PhaseShared phs;
+  __shared__ typename G::Shared gsh;
+  __shared__ typename Mdl::Shared msh;
+  const bool producer = threadIdx.x < TILE;
+  const int gdims = Mdl::gen_dims(a.mp.dim);
+  const int nchunk = gdims > 0 ? (gdims + CHUNK - 1) / CHUNK : 1;
+  const int total = a.rep_n * (int)a.tiles_per_rep;
+  if ((int)blockIdx.x >= total) return;
+  const bool contiguous = nchunk == 1;
+  const int nb = gridDim.x, b = blockIdx.x;
+  const int lo = contiguous ? (int)((int64_t)total * b / nb) : b;
+  const int ntile =
+      contiguous ? (int)((int64_t)total * (b + 1) / nb) - lo : (total - b + nb - 1) / nb;
+  const int nunit = ntile * nchunk;
+  const int tpr = (int)a.tiles_per_rep;
+  const int tstride = contiguous ? 1 : nb;
+  struct Cursor {
+    int rl, c, tile;
+  };
+  auto advance = [&](Cursor &q) {
+    if (++q.c == nchunk) {
+      q.c = 0;
+      q.tile += tstride;
+      while (q.tile >= tpr) {
+        q.tile -= tpr;
+        q.rl++;
+      }
+    }
+  };
+  Cursor cur{a.rep_local0 + lo / tpr, 0, lo % tpr};
+  auto dc_of = [&](int c) { return gdims - c * CHUNK < CHUNK ? gdims - c * CHUNK : CHUNK; };
+  if (producer) {
+    const int warp = threadIdx.x >> 5;
+    G g;
+    g.setup(a.t, gsh, gdims);
+    give_phase(g, phs);
+    nbar_sync<BAR_PROD, TILE>();
+    for (int u = 0; u < nunit; u++) {
+      const int buf = u & 1;
+      double *zb = z + buf * (CHUNK * TILE);
+      const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
+      const int64_t base = (int64_t)cur.tile * TILE;
+      if (u >= 2) {  // the consumers are done with zb
+        if (buf) nbar_sync<BAR_EMPTY0 + 1, 2 * TILE>();
+        else nbar_sync<BAR_EMPTY0, 2 * TILE>();
+      }
+      if (gdims > 0) {
+        g.unit(rl, (uint64_t)base, (uint64_t)(base + threadIdx.x), d0, Dc, zb);
+        nbar_sync<BAR_PROD, TILE>();  // every dim of the unit is in zb
+      }
+      if (Mdl::NORMALS)
+        chunk_to_normals<FixedDims<Mdl>::value, std::is_same<G, GenRasrapRecTile<true>>::value>(
+            zb, Dc, phs.tq[warp]);
+      if (buf) nbar_arrive<BAR_FULL0 + 1, 2 * TILE>();
+      else nbar_arrive<BAR_FULL0, 2 * TILE>();
+      advance(cur);
+    }
+  } else {
+    Mdl md;
+    md.init(a.mp, msh);
+    ModelDyn<Mdl>::give(md, z + 2 * CHUNK * TILE);
+    nbar_sync<BAR_CONS, TILE>();
+    const int t = ctid();
+    for (int u = 0; u < nunit; u++) {
+      const int buf = u & 1;
+      const double *zb = z + buf * (CHUNK * TILE);
+      const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
+      const int64_t base = (int64_t)cur.tile * TILE;
+      if (buf) nbar_sync<BAR_FULL0 + 1, 2 * TILE>();  // the producers filled zb
+      else nbar_sync<BAR_FULL0, 2 * TILE>();
+      if (d0 == 0) md.begin();
+      md.chunk(d0, Dc, zb + t);
+      if (d0 + Dc >= gdims) {
+        const int64_t path = base + t;
+        if (path < a.nmax)
+          a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.payoff();
+      }
+      if (buf) nbar_arrive<BAR_EMPTY0 + 1, 2 * TILE>();
+      else nbar_arrive<BAR_EMPTY0, 2 * TILE>();
+      advance(cur);
+    }
+  }
+}
+
+// ======================================================================
 // Path kernel of the sequential word streams (MT19937 / XORWOW).  Units of
 // work are (replication, segment of seg_len paths); a CTA walks its units
 // grid-stride.  Per unit the generator is positioned once (snapshot load or
@@ -2370,9 +2563,7 @@ __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_
   double acc = 0.0;
   int qn = 0;
   auto tail_one = [&](int i) {
-    bool neg;
-    const double x0 = invn_tail(invn_fold(qv[warp][i], &neg));
-    const double x = neg ? -x0 : x0;
+    const double x = invn_queued(qv[warp][i]);  // tail candidates: exact test, then tail
     acc += x;
     if constexpr (STORE) store[qs[warp][i]] = x;
   };
@@ -2388,7 +2579,7 @@ __global__ void __launch_bounds__(TILE) k_stream_reg(RepTables t, int rl, int64_
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         use[k] = ok && (whole || d0 + k < t.dim);
-        tail[k] = use[k] && invn_tail_p(u[k]);
+        tail[k] = use[k] && (RQ_TAIL_CAND ? invn_tail_cand(u[k]) : invn_tail_p(u[k]));
       }
 #pragma unroll
       for (int k = 0; k < 4; k++) x[k] = invn_central_q(u[k] - 0.5);
@@ -2652,6 +2843,28 @@ template <class G, class Mdl>
 static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                             int *blocks_out) {
   const int64_t work = (int64_t)a.rep_n * a.tiles_per_rep;
+#if RQ_WS
+  // generators whose unit has no CTA-wide barrier (the consumer warpgroup
+  // never reaches one: GenRasrapCounterTile syncs the whole CTA); RQ_WS = 1:
+  // only where it measured faster (the persistent Rasrap tile with LIBOR
+  // S <= 20), 2: every eligible pair (experiments)
+  constexpr bool ws_ok = !std::is_same<G, GenRasrapCounterTile>::value;
+  constexpr bool ws_pick = RQ_WS >= 2 || (std::is_same<G, GenRasrapRecTile<true>>::value &&
+                                          Mdl::SMALL_LIBOR);
+  if constexpr (ws_ok && ws_pick) {
+    size_t dyn = prep_dyn(k_paths_ws<G, Mdl>, 2 * ZT_BYTES + ModelDyn<Mdl>::bytes(a.mp.dim));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_paths_ws<G, Mdl>, 2 * TILE, dyn);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t bmax = (int64_t)per_sm * sm_count();
+    const int blocks = (int)(work < bmax ? (work < 1 ? 1 : work) : bmax);
+    if (blocks_out) *blocks_out = blocks;
+    if (probe) return cudaSuccess;
+    k_paths_ws<G, Mdl><<<blocks, 2 * TILE, dyn, s>>>(a);
+    if (launched) *launched += 1;
+    return cudaGetLastError();
+  }
+#endif
   size_t dyn = prep_dyn(k_paths<G, Mdl>, ZT_BYTES + ModelDyn<Mdl>::bytes(a.mp.dim));
   int blocks = persistent_blocks(k_paths<G, Mdl>, work, dyn);
   if (blocks_out) *blocks_out = blocks;

@@ -1,7 +1,8 @@
-# quick GPU check: parity tests + short benches of the main workloads
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
+# Quick check after a kernel change: Rasrap parity subset + short bench lines.
+mkdir -p gpurun_out
 rm -f gpurun_out/quick.json
-for w in c2 c3 c5; do timeout 300 python bench.py --workload $w --no-cpu-baseline --steps 3 $([ $w != c2 ] && echo --reps 64) >> gpurun_out/quick.json 2>>gpurun_out/quick.err; done
-timeout 300 python bench.py --generator philox --no-cpu-baseline --steps 3 >> gpurun_out/quick.json 2>>gpurun_out/quick.err
-for g in philox rasrap-recursive; do timeout 300 python bench.py --workload c4 --generator $g --steps 3 >> gpurun_out/quick.json 2>>gpurun_out/quick.err; done
+timeout 900 python -m pytest tests -m gpu -q -x -k "${TESTK:-rasrap or xhash or c2_ or c3_ or c5_}" > gpurun_out/quick_tests.log 2>&1; echo tests=$?; tail -3 gpurun_out/quick_tests.log
+for wl in ${WLS:-"c2" "c3 --reps 64" "c5 --reps 128" "c4"}; do
+  timeout 300 python bench.py --workload $wl --generator ${GEN:-rasrap-recursive} --no-cpu-baseline --steps 3 >> gpurun_out/quick.json 2>>gpurun_out/quick.err
+done
 python tools/bench_table.py gpurun_out/quick.json
