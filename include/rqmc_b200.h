@@ -92,6 +92,15 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
                       int64_t rep_first, int32_t rep_count, void *stream);
 void rq_sampler_destroy(rq_sampler *s);
 
+/* Exclusive upper bound on point indices the device evaluates for a
+ * generator (the reference takes int64 indices: RasrapCounter.at
+ * halton.py:506-512, the Philox counter's path_hi prng.py:180-246):
+ * 2^62 for Philox and SFC64, 2^39 for both Rasrap forms (n0 + i stays inside
+ * the digit window, >= 2^40 for every base), 2^32 for Sobol' (32-bit
+ * direction numbers: sobol.py:181-193 raises beyond) and for the sequential
+ * word streams / Kakutani orbits.  Larger indices return RQ_ERR_RANGE. */
+int64_t rq_index_limit(int generator);
+
 /* sampler.fill(out) for rows first..first+count-1 of replication
  * rep_first+rep_local (halton.py:479, sobol.py:341, harness.py:63):
  * out_dev[count][dim] row-major float64. */

@@ -74,6 +74,8 @@ def _declare(L):
     L.rq_sampler_destroy.restype = None
     L.rq_sampler_points.argtypes = [vp, i32, i64, i64, vp, vp]
     L.rq_sampler_points_at.argtypes = [vp, i32, vp, i64, vp, vp]
+    L.rq_index_limit.restype = i64
+    L.rq_index_limit.argtypes = [C.c_int]
     L.rq_sampler_rasrap_tables.argtypes = [vp, i32, vp, vp, vp]
     L.rq_estimate.argtypes = [vp, P(RqModel), P(i64), i32, vp, P(i32), vp]
     L.rq_run_replications.argtypes = [C.c_int, P(RqModel), u64, i64, i64, P(i64), i32, P(dbl),

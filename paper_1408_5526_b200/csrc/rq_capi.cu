@@ -30,6 +30,12 @@ struct Stats {
   int64_t paths_launches = 0;
 } g_stats;
 std::mutex g_stats_mu;
+// counters may be bumped from several host threads (one per device)
+template <class T>
+void stat_add(T &field, T v) {
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  field += v;
+}
 
 struct KTimer {  // CUDA events on the launching stream when timing is on
   cudaEvent_t a = nullptr, b = nullptr;
@@ -48,7 +54,7 @@ struct KTimer {  // CUDA events on the launching stream when timing is on
       cudaEventSynchronize(b);
       float ms = 0;
       cudaEventElapsedTime(&ms, a, b);
-      *acc += ms;
+      stat_add(*acc, (double)ms);
       cudaEventDestroy(a);
       cudaEventDestroy(b);
     }
@@ -431,16 +437,34 @@ void build_plan(int64_t n, HostPlan &P) {
   P.nnodes = L + I;
 }
 
+// Stream-ordered device allocation released when it goes out of scope, so
+// the early error returns of the entry points leak nothing.
+struct DevMem {
+  void *p = nullptr;
+  cudaStream_t s = nullptr;
+  DevMem() = default;
+  explicit DevMem(cudaStream_t s_) : s(s_) {}
+  DevMem(const DevMem &) = delete;
+  DevMem &operator=(const DevMem &) = delete;
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+  template <class T>
+  T *as() const { return (T *)p; }
+  ~DevMem() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 struct DevPlan {
   rq::SumPlan p{};
-  void *buf = nullptr;
+  DevMem buf;
 };
 
 int upload_plan(const HostPlan &hp, DevPlan &dp, cudaStream_t s) {
   size_t nl = hp.leaf_start.size(), ni = hp.node_id.size(), nlev = hp.level_off.size();
   size_t bytes = nl * 8 + nl * 4 + nlev * 4 + 3 * ni * 4 + 64;
-  RQ_CUDA(cudaMallocAsync(&dp.buf, bytes, s));
-  char *b = (char *)dp.buf;
+  dp.buf.s = s;
+  RQ_CUDA(dp.buf.alloc(bytes));
+  char *b = dp.buf.as<char>();
   std::vector<char> host(bytes);
   size_t off = 0;
   auto put = [&](const void *src, size_t n) {
@@ -460,8 +484,8 @@ int upload_plan(const HostPlan &hp, DevPlan &dp, cudaStream_t s) {
   dp.p.node_id = (const int32_t *)put(hp.node_id.data(), ni * 4);
   dp.p.node_l = (const int32_t *)put(hp.node_l.data(), ni * 4);
   dp.p.node_r = (const int32_t *)put(hp.node_r.data(), ni * 4);
-  RQ_CUDA(cudaMemcpyAsync(dp.buf, host.data(), off, cudaMemcpyHostToDevice, s));
-  g_stats.h2d += off;
+  RQ_CUDA(cudaMemcpyAsync(dp.buf.p, host.data(), off, cudaMemcpyHostToDevice, s));
+  stat_add(g_stats.h2d, (uint64_t)off);
   // the host staging buffer must outlive the copy
   RQ_CUDA(cudaStreamSynchronize(s));
   return RQ_OK;
@@ -597,7 +621,7 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
     uint32_t *gen = vd + (size_t)dim * 32;
     uint32_t *sh = gen + (size_t)dim * 32 * rep_count;
     e = cudaMemcpyAsync(vd, v.data(), b_v, cudaMemcpyHostToDevice, s);
-    g_stats.h2d += b_v;
+    stat_add(g_stats.h2d, (uint64_t)b_v);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // v is a host temporary
     if (e == cudaSuccess) {
       KTimer kt(&g_stats.setup_ms, s);
@@ -725,13 +749,25 @@ static int check_rep(rq_sampler *s, int32_t rl) {
   return RQ_OK;
 }
 
+int64_t rq_index_limit(int generator) {
+  switch (generator) {
+    case rq::GEN_PHILOX:
+    case rq::GEN_SFC64: return (int64_t)1 << 62;
+    case rq::GEN_RASRAP_RECURSIVE:
+    case rq::GEN_RASRAP_COUNTER: return (int64_t)1 << 39;
+  }
+  return (int64_t)1 << 32;
+}
+
 int rq_sampler_points(rq_sampler *s, int32_t rep_local, int64_t first, int64_t count,
                       double *out_dev, void *stream) {
   int rc = check_rep(s, rep_local);
   if (rc) return rc;
   if (first < 0 || count < 0) return fail(RQ_ERR_VALUE, "index must be non-negative");
-  if (first + count > (int64_t)1 << 32)
-    return fail(RQ_ERR_RANGE, "point index %lld exceeds 2^32", (long long)(first + count));
+  const int64_t lim = rq_index_limit(s->t.gen);
+  if (first > lim || count > lim - first)
+    return fail(RQ_ERR_RANGE, "point index %lld exceeds the generator's index range %lld",
+                (long long)(first + count), (long long)lim);
   if (count == 0) return RQ_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (rq::gen_sequential(s->t.gen)) {  // _WordSampler.fill: words from the cursor on
@@ -780,7 +816,7 @@ int rq_sampler_rasrap_tables(rq_sampler *s, int32_t rep_local, uint16_t *digits_
   return RQ_OK;
 }
 
-static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, double **tab_dev,
+static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, DevMem &tab,
                            cudaStream_t s) {
   if (!m) return fail(RQ_ERR_VALUE, "model is NULL");
   if (m->kind < 0 || m->kind == rq::MODEL_POINTS || m->kind > rq::MODEL_XHASH)
@@ -810,13 +846,13 @@ static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, doub
   }
   mp.exp_zlim = m->sigma_xi > 0.0 ? 0.1 / m->sigma_xi : INFINITY;
   mp.table = nullptr;
-  *tab_dev = nullptr;
   if (m->kind == rq::MODEL_LIBOR || m->kind == rq::MODEL_MBS) {
     if (!m->table) return fail(RQ_ERR_VALUE, "model table is NULL");
-    RQ_CUDA(cudaMallocAsync((void **)tab_dev, sizeof(double) * m->dim, s));
-    RQ_CUDA(cudaMemcpyAsync(*tab_dev, m->table, sizeof(double) * m->dim, cudaMemcpyHostToDevice, s));
-    g_stats.h2d += sizeof(double) * m->dim;
-    mp.table = *tab_dev;
+    tab.s = s;
+    RQ_CUDA(tab.alloc(sizeof(double) * m->dim));
+    RQ_CUDA(cudaMemcpyAsync(tab.p, m->table, sizeof(double) * m->dim, cudaMemcpyHostToDevice, s));
+    stat_add(g_stats.h2d, (uint64_t)(sizeof(double) * m->dim));
+    mp.table = tab.as<double>();
   }
   return RQ_OK;
 }
@@ -838,12 +874,13 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   rq::ModelParams mp;
-  double *tab = nullptr;
-  if ((rc = model_to_params(model, s->t.dim, mp, &tab, st))) return rc;
+  DevMem tab;
+  if ((rc = model_to_params(model, s->t.dim, mp, tab, st))) return rc;
   const int64_t nmax = grid_host[ngrid - 1];
   // replication batch: payoff buffer <= 1 GiB (2^27 paths), >= 1 replication
   int64_t B = std::max<int64_t>(1, env_int("RQ_BATCH_PATHS", (int64_t)128 << 20) / nmax);
   B = std::min<int64_t>(B, s->t.rep_count);
+  B = std::min<int64_t>(B, 65535);  // the reduction's grid.y
   std::vector<HostPlan> hplans(ngrid);
   std::vector<DevPlan> dplans(ngrid);
   int32_t maxnodes = 1;
@@ -852,11 +889,12 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
     maxnodes = std::max(maxnodes, hplans[g].nnodes);
     if ((rc = upload_plan(hplans[g], dplans[g], st))) return rc;
   }
-  double *pay = nullptr, *scratch = nullptr;
-  unsigned *tickets = nullptr;
-  RQ_CUDA(cudaMallocAsync((void **)&pay, sizeof(double) * B * nmax, st));
-  RQ_CUDA(cudaMallocAsync((void **)&scratch, sizeof(double) * B * maxnodes, st));
-  RQ_CUDA(cudaMallocAsync((void **)&tickets, sizeof(unsigned) * B, st));
+  DevMem pay_m(st), scratch_m(st), tickets_m(st);
+  RQ_CUDA(pay_m.alloc(sizeof(double) * B * nmax));
+  RQ_CUDA(scratch_m.alloc(sizeof(double) * B * maxnodes));
+  RQ_CUDA(tickets_m.alloc(sizeof(unsigned) * B));
+  double *pay = pay_m.as<double>(), *scratch = scratch_m.as<double>();
+  unsigned *tickets = tickets_m.as<unsigned>();
   RQ_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * B, st));
   int launched = 0;
   SeqRun R;
@@ -870,11 +908,11 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
       if ((rc = seq_batch(s->t, (int)r0, rn, R, &blocks, &launched, st))) return rc;
       KTimer kt(&g_stats.paths_ms, st);
       e = rq::launch_paths_seq(s->t, mp, (int)r0, rn, nmax, R.q, blocks, pay, &launched, st);
-      g_stats.paths_launches++;
+      stat_add(g_stats.paths_launches, (int64_t)1);
     } else {
       KTimer kt(&g_stats.paths_ms, st);
       e = rq::launch_paths(s->t, mp, (int)r0, rn, nmax, pay, &launched, st);
-      g_stats.paths_launches++;
+      stat_add(g_stats.paths_launches, (int64_t)1);
     }
     if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "path kernel: %s", cudaGetErrorString(e));
     for (int g = 0; g < ngrid; g++) {
@@ -885,13 +923,25 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
       launched++;
     }
   }
-  cudaFreeAsync(pay, st);
-  cudaFreeAsync(scratch, st);
-  cudaFreeAsync(tickets, st);
-  if (tab) cudaFreeAsync(tab, st);
-  for (auto &d : dplans) cudaFreeAsync(d.buf, st);
   if (kernel_launches) *kernel_launches += launched;
   return RQ_OK;
+}
+
+// Device table bytes of one replication's randomisation (rq_sampler_create).
+static size_t sampler_bytes_per_rep(int generator, int dim) {
+  if (dim < 1) return 64;
+  const HostTables &T = host_tables();
+  switch (generator) {
+    case rq::GEN_RASRAP_RECURSIVE:
+    case rq::GEN_RASRAP_COUNTER:
+      if (dim > rq::MAX_DIM) return 64;
+      return 2 * (size_t)T.total_bases(dim) + 8 * (size_t)T.total_sums(dim) +
+             2 * (size_t)T.total_caps(dim) + 8 * (size_t)dim + 64;
+    case rq::GEN_SOBOL_GRAY:
+    case rq::GEN_SOBOL_COUNTER: return 4 * 33 * (size_t)dim + 64;
+    case rq::GEN_KAKUTANI: return 8 * (size_t)dim + 64;
+  }
+  return 64;
 }
 
 int rq_run_replications(int generator, const rq_model *model, uint64_t seed, int64_t rep_first,
@@ -913,27 +963,29 @@ int rq_run_replications(int generator, const rq_model *model, uint64_t seed, int
     if (!streams[dev]) RQ_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
     st = streams[dev];
   }
-  double *theta_dev = nullptr;
-  RQ_CUDA(cudaMallocAsync((void **)&theta_dev, sizeof(double) * rep_count * ngrid, st));
-  // replication groups bound the randomisation tables (<= ~256 MiB)
-  const int64_t G = 4096;
+  DevMem theta_m(st);
+  RQ_CUDA(theta_m.alloc(sizeof(double) * rep_count * ngrid));
+  double *theta_dev = theta_m.as<double>();
+  // replication groups bound the randomisation tables to ~256 MiB
+  const int dim = model ? model->dim : 0;
+  const int64_t G = std::max<int64_t>(
+      1, std::min<int64_t>(4096, ((int64_t)256 << 20) / (int64_t)sampler_bytes_per_rep(generator, dim)));
   for (int64_t r0 = 0; r0 < rep_count; r0 += G) {
     int32_t rn = (int32_t)std::min<int64_t>(G, rep_count - r0);
     rq_sampler *S = nullptr;
-    if ((rc = rq_sampler_create(&S, generator, model ? model->dim : 0, seed, rep_first + r0, rn, st)))
-      return rc;
+    if ((rc = rq_sampler_create(&S, generator, dim, seed, rep_first + r0, rn, st))) return rc;
     if (kernel_launches && generator != rq::GEN_PHILOX && generator != rq::GEN_SFC64 &&
         generator != rq::GEN_TWISTER)  // (kakutani / xorwow: their start kernels)
       *kernel_launches += 1;  // the randomisation setup kernel
     rc = rq_estimate(S, model, grid_host, ngrid, theta_dev + r0 * ngrid, kernel_launches, st);
-    RQ_CUDA(cudaStreamSynchronize(st));
+    const cudaError_t e = cudaStreamSynchronize(st);
     rq_sampler_destroy(S);
     if (rc) return rc;
+    if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "%s", cudaGetErrorString(e));
   }
   RQ_CUDA(cudaMemcpyAsync(theta_host, theta_dev, sizeof(double) * rep_count * ngrid,
                           cudaMemcpyDeviceToHost, st));
-  g_stats.d2h += sizeof(double) * rep_count * ngrid;
-  RQ_CUDA(cudaFreeAsync(theta_dev, st));
+  stat_add(g_stats.d2h, (uint64_t)(sizeof(double) * rep_count * ngrid));
   RQ_CUDA(cudaStreamSynchronize(st));
   for (int64_t k = 0; k < rep_count * ngrid; k++)
     if (!std::isfinite(theta_host[k]))
@@ -947,13 +999,12 @@ int rq_model_payoffs(const rq_model *model, const double *u_dev, int64_t npaths,
   if (!model) return fail(RQ_ERR_VALUE, "model is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   rq::ModelParams mp;
-  double *tab = nullptr;
-  int rc = model_to_params(model, model->dim, mp, &tab, st);
+  DevMem tab;
+  int rc = model_to_params(model, model->dim, mp, tab, st);
   if (rc) return rc;
   if (mp.kind != rq::MODEL_LIBOR && mp.kind != rq::MODEL_MBS)
     return fail(RQ_ERR_VALUE, "payoff kernel only for libor/mbs");
   RQ_CUDA(rq::launch_model_payoffs(mp, u_dev, npaths, out_dev, st));
-  if (tab) cudaFreeAsync(tab, st);
   return RQ_OK;
 }
 
@@ -971,21 +1022,22 @@ int rq_stream_normals(rq_sampler *s, int32_t rep_local, int64_t npoints, double 
     return fail(RQ_ERR_VALUE, "the normals stream is for counter/QMC generators (config 4)");
   cudaStream_t st = (cudaStream_t)stream;
   int blocks = rq::stream_grid_blocks(s->t);
-  double *bs = nullptr;
-  RQ_CUDA(cudaMallocAsync((void **)&bs, sizeof(double) * blocks, st));
+  DevMem bs_m(st);
+  RQ_CUDA(bs_m.alloc(sizeof(double) * blocks));
+  double *bs = bs_m.as<double>();
   RQ_CUDA(rq::launch_stream_normals(s->t, rep_local, npoints, bs, blocks, store_dev, st));
-  rc = rq_pairwise_sum(bs, blocks, sum_dev, stream);
-  cudaFreeAsync(bs, st);
-  return rc;
+  return rq_pairwise_sum(bs, blocks, sum_dev, stream);
 }
 
 void rq_stats_reset(int timing) {
+  std::lock_guard<std::mutex> lk(g_stats_mu);
   g_stats = Stats();
   g_stats.timing = timing != 0;
 }
 
 void rq_stats_get(uint64_t *h2d, uint64_t *d2h, double *setup_ms, double *paths_ms,
                   double *reduce_ms, int64_t *paths_launches) {
+  std::lock_guard<std::mutex> lk(g_stats_mu);
   if (h2d) *h2d = g_stats.h2d;
   if (d2h) *d2h = g_stats.d2h;
   if (setup_ms) *setup_ms = g_stats.setup_ms;
@@ -1062,17 +1114,15 @@ int rq_pairwise_sum(const double *a_dev, int64_t n, double *out_dev, void *strea
   DevPlan dp;
   int rc = upload_plan(hp, dp, st);
   if (rc) return rc;
-  double *scratch = nullptr;
-  unsigned *tickets = nullptr;
-  RQ_CUDA(cudaMallocAsync((void **)&scratch, sizeof(double) * hp.nnodes, st));
-  RQ_CUDA(cudaMallocAsync((void **)&tickets, sizeof(unsigned), st));
+  DevMem scratch_m(st), tickets_m(st);
+  RQ_CUDA(scratch_m.alloc(sizeof(double) * hp.nnodes));
+  RQ_CUDA(tickets_m.alloc(sizeof(unsigned)));
+  double *scratch = scratch_m.as<double>();
+  unsigned *tickets = tickets_m.as<unsigned>();
   RQ_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned), st));
   // theta = sum / n: multiply back by n is not exact, so reduce with n = 1 divisor
   dp.p.n = 1;
   RQ_CUDA(rq::launch_reduce(dp.p, a_dev, n, 1, out_dev, 1, scratch, tickets, st));
-  cudaFreeAsync(scratch, st);
-  cudaFreeAsync(tickets, st);
-  cudaFreeAsync(dp.buf, st);
   return RQ_OK;
 }
 

@@ -224,6 +224,7 @@ struct RasrapTileShared {
   int32_t hB[CHUNK];               // highest digit where B differs from n0 (-1: B == n0)
   double sJ[CHUNK];                // stream partial sum S_J of the top node
   int32_t st_rl[CHUNK];            // replication the state belongs to (-1: none)
+  int32_t stg_rl[WARPS];           // replication whose sigma a warp staged (warp-private)
   uint64_t st_base[CHUNK];         // tile base the state belongs to
   int32_t soff[CHUNK];             // offset of sigma_d in sigd
 };
@@ -290,18 +291,21 @@ __device__ __forceinline__ void give_phase(G &g, PhaseShared &p) {
 // then holds sums[j] = init_sums[j] above h and the chain
 // S_j = S_{j+1} + sigma(a_j) * binpow(1/p, j+1) below, so the point is that
 // chain started from init_sums[h+1] -- bit-identical to the reference.
-__device__ double rasrap_rec_direct(const RepTables &t, int rl, int d, uint32_t i,
+// Indices are 64-bit: n = n0 + i stays inside the digit window (p^(K+8) >=
+// 2^40) for i < RQ_RASRAP_INDEX_MAX (2^39, checked by the C ABI).
+__device__ double rasrap_rec_direct(const RepTables &t, int rl, int d, uint64_t i,
                                     uint16_t *scr) {
   const HaltonDim &h = c_hdim[d];
   const uint16_t *d0 = t.digits + (int64_t)rl * t.dig_stride + h.dig_off;
   const uint16_t *sg = t.sigma + (int64_t)rl * t.sig_stride + h.sig_off;
   const double *sums = t.sums + (int64_t)rl * t.sum_stride + h.sum_off;
-  uint32_t r = i, carry = 0;
+  uint64_t r = i;
+  uint32_t carry = 0;
   int hi = -1, j = 0;
   while (r != 0u || carry != 0u) {
-    uint32_t q = div_base(r, h);
+    const uint64_t q = r >> 32 ? div_base64(r, h) : (uint64_t)div_base((uint32_t)r, h);
     uint32_t a0 = d0[j];
-    uint32_t a = a0 + (r - q * (uint32_t)h.base) + carry;
+    uint32_t a = a0 + (uint32_t)(r - q * (uint64_t)h.base) + carry;
     carry = a >= (uint32_t)h.base;
     a = carry ? a - (uint32_t)h.base : a;
     scr[j * TILE] = (uint16_t)a;
@@ -326,7 +330,7 @@ struct GenRasrapRecDirect {
   __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
     uint16_t *scr = &sh->scr[0][0] + threadIdx.x;
     for (int dd = 0; dd < Dc; dd++)
-      zt[dd * TILE + threadIdx.x] = rasrap_rec_direct(*t, rl, d0 + dd, (uint32_t)path, scr);
+      zt[dd * TILE + threadIdx.x] = rasrap_rec_direct(*t, rl, d0 + dd, path, scr);
   }
 };
 
@@ -367,6 +371,7 @@ struct GenRasrapRecTile {
     t = &t_;
     sh = &s;
     for (int k = threadIdx.x; k < CHUNK; k += TILE) s.st_rl[k] = -1;
+    for (int k = threadIdx.x; k < WARPS; k += TILE) s.stg_rl[k] = -1;
   }
   // Full state at B = n0 + base: digits, hB, P[j] = S_j(B) (chain from
   // init_sums[hB+1]); used for a CTA's first tile of a replication.
@@ -582,9 +587,10 @@ struct GenRasrapRecTile {
   __device__ void unit(int rl, uint64_t base, uint64_t, int d0, int Dc, double *zt) {
     RasrapTileShared &R = *sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (sig_smem) {
-      const int d1 = dim_slot(warp, 0, d0, Dc);
-      if (R.st_rl[d1 < 0 ? 0 : d1] != rl) stage_sigma(rl, d0, Dc);
+    if (sig_smem && R.stg_rl[warp] != rl) {  // warp-private flag: no cross-warp read
+      stage_sigma(rl, d0, Dc);
+      __syncwarp();  // every lane has read the flag before lane 0 rewrites it
+      if (lane == 0) R.stg_rl[warp] = rl;
     }
     {  // lane k prepares the dim of slot k (base 2: no tree state)
       const int dd = dim_slot(warp, lane, d0, Dc);
@@ -703,19 +709,19 @@ struct GenRasrapCounter {
   __device__ void unit(int rl, uint64_t, uint64_t path, int d0, int Dc, double *zt) {
     const uint16_t *dig = t->digits + (int64_t)rl * t->dig_stride;
     const uint16_t *sig = t->sigma + (int64_t)rl * t->sig_stride;
-    const uint32_t i = (uint32_t)path;
 #pragma unroll 1
     for (int dd = 0; dd < Dc; dd++) {
       const HaltonDim &h = c_hdim[d0 + dd];
       const uint16_t *n0d = dig + h.dig_off;
       const uint16_t *sg = sig + h.sig_off;
       const double *cs = g_cscale + h.sum_off;
-      uint32_t r = i, carry = 0;
+      uint64_t r = path;  // 64-bit index (halton.py:506-512 takes int64)
+      uint32_t carry = 0;
       double x = 0.0;
 #pragma unroll 1
       for (int j = 0; j < h.K || r != 0u || carry != 0u; j++) {
-        uint32_t q = div_base(r, h);
-        uint32_t a = n0d[j] + (r - q * (uint32_t)h.base) + carry;
+        const uint64_t q = r >> 32 ? div_base64(r, h) : (uint64_t)div_base((uint32_t)r, h);
+        uint32_t a = n0d[j] + (uint32_t)(r - q * (uint64_t)h.base) + carry;
         carry = a >= (uint32_t)h.base;
         a = carry ? a - (uint32_t)h.base : a;
         x = dadd(x, dmul(u16d(sg[a]), cs[j]));
@@ -735,7 +741,7 @@ struct GenRasrapCounter {
 // T_j = s(a_j) w_j of its H (the same products, rounded the same way) are
 // formed once per tile and dim and then added in order: bit-identical, with
 // L instead of max(K, #digits) digit extractions per point.
-constexpr int CT_MAXT = 36;  // high terms per variant (K - L + overflow digits <= 32)
+constexpr int CT_MAXT = 40;  // high terms per variant (digits of n >> L, n < 2^46)
 struct GenRasrapCounterTile {
   static constexpr int MAXB = 4;
   struct Shared {
@@ -1005,6 +1011,7 @@ struct GenSobolTileP {
         R.H[dd] = sobol_word<false>(v + (d0 + dd) * SOBOL_BITS, __ldg(shp + d0 + dd),
                                     (uint64_t)gT << 7);
     }
+    __syncwarp();  // every lane has read st_rl / st_T before lane 0 rewrites them
     if (lane == 0) {
       R.st_rl[warp] = rl;
       R.st_T[warp] = T;

@@ -47,15 +47,19 @@ class DeviceSampler:
         self._h = h
         self._torch = torch
 
-    def __del__(self):
+    def close(self) -> None:
+        """Release the device tables now (also done when the object dies)."""
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            try:
-                self._torch.cuda.current_stream().synchronize()
-                _lib.lib().rq_sampler_destroy(h)
-            except Exception:  # pragma: no cover - interpreter shutdown
-                pass
-            self._h = None
+            self._torch.cuda.current_stream().synchronize()
+            _lib.lib().rq_sampler_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
 
     # -- device-level API -------------------------------------------------
     def points(self, first: int, count: int):
@@ -72,10 +76,12 @@ class DeviceSampler:
             indices, torch.Tensor) else indices, dtype=torch.int64).to("cuda").contiguous()
         if idx.numel() and int(idx.min()) < 0:
             raise ValueError("index must be non-negative")
-        if idx.numel() and int(idx.max()) >= 2**32:
+        lim = int(_lib.lib().rq_index_limit(_lib.GEN_IDS[self.name]))
+        if idx.numel() and int(idx.max()) >= lim:
             from .harness import ConfigurationError
 
-            raise ConfigurationError("point index exceeds 2^32 (device index range)")
+            raise ConfigurationError(f"point index exceeds the device index range of "
+                                     f"{self.name} ({lim})")
         out = torch.empty((idx.numel(), self.dim), dtype=torch.float64, device="cuda")
         _lib.check(_lib.lib().rq_sampler_points_at(self._h, 0, idx.data_ptr(), idx.numel(),
                                                     out.data_ptr(), _lib.stream_ptr()))

@@ -57,10 +57,10 @@ def test_rasrap_points_bit_exact(P, golden, tag, form):
     rows = g[f"{tag}_rows"]
     got = s.points_at(rows).cpu().numpy()
     assert np.array_equal(got, g[f"{tag}_{form}"])
-    if form == "counter":
+    if form == "counter":  # indices up to 3 * 2^33 + 5 (RasrapCounter.at on int64)
         big = g[f"{tag}_bigidx"]
-        ok = big < 2**32
-        assert np.array_equal(s.points_at(big[ok]).cpu().numpy(), g[f"{tag}_counter_big"][ok])
+        assert big.max() > 2**34
+        assert np.array_equal(s.points_at(big).cpu().numpy(), g[f"{tag}_counter_big"])
 
 
 @pytest.mark.parametrize("tag", ["d20_m1", "d80_m3", "d360_m2"])
@@ -167,10 +167,56 @@ def test_large_index_blocks_match_oracle(P, oracle, gen):
         assert np.array_equal(got, ref)
 
 
-def test_index_beyond_2_32_rejected(P):
-    s = P.make_sampler("philox", 4, SEED, 1)
+def test_index_range_per_generator(P):
+    """Sobol' stops at 2^32 (32-bit direction numbers; sobol.py:181-193
+    raises), the counter PRNGs and Rasrap take 64-bit indices."""
+    from paper_1408_5526_b200 import _lib
+
+    lim = {g: int(_lib.lib().rq_index_limit(i)) for g, i in _lib.GEN_IDS.items()}
+    assert lim["sobol-gray"] == lim["sobol-counter"] == 2**32
+    assert lim["philox"] == lim["sfc64"] == 2**62
+    assert lim["rasrap-recursive"] == lim["rasrap-counter"] == 2**39
+    s = P.make_sampler("sobol-gray", 4, SEED, 1)
     with pytest.raises(ValueError):
         s.points(2**32 - 2, 5)
+    with pytest.raises(ValueError):
+        P.make_sampler("rasrap-counter", 4, SEED, 1).at(np.array([2**39]))
+    assert P.make_sampler("philox", 4, SEED, 1).points(2**32 - 2, 5).shape == (5, 4)
+
+
+@pytest.mark.parametrize("gen", ["philox", "sfc64", "rasrap-counter", "rasrap-recursive"])
+def test_64bit_indices_match_oracle(P, oracle, gen):
+    """Points at indices beyond 2^32 (the reference takes int64 indices:
+    halton.py:506-512, prng.py:180-246) vs the oracle, through at() (direct
+    kernels) and fill() (tile kernels) across the 2^32 boundary."""
+    from paper_1408_5526_b200.samplers import DeviceSampler
+
+    dim, m = 20, 3
+    s = DeviceSampler(gen, dim, SEED, m)
+    hi = 2**61 if gen in ("philox", "sfc64") else 2**39
+    idx = np.concatenate([np.arange(2**32 - 70, 2**32 + 70), np.arange(2**36 - 5, 2**36 + 5),
+                          np.arange(hi - 40, hi)]).astype(np.int64)
+    got = s.points_at(idx).cpu().numpy()
+    run = s.points(2**32 - 300, 600).cpu().numpy()  # fill across the 2^32 boundary
+    ridx = np.arange(2**32 - 300, 2**32 + 300, dtype=np.int64)
+    if gen == "philox":
+        key = oracle.derive_key(SEED, 3, m)
+        words = lambda ix: oracle.philox_words(key, ix, dim) * 2.0**-32 + 2.0**-33  # noqa: E731
+        assert np.array_equal(got, words(idx))
+        assert np.array_equal(run, words(ridx))
+    elif gen == "sfc64":
+        assert np.array_equal(got, oracle.sfc64_uniforms(SEED, m, idx, dim))
+        assert np.array_equal(run, oracle.sfc64_uniforms(SEED, m, ridx, dim))
+    else:
+        key = oracle.derive_key(SEED, 4, m)
+        ref, rref = oracle.rasrap_counter(dim, key, idx), oracle.rasrap_counter(dim, key, ridx)
+        if gen == "rasrap-counter":
+            assert np.array_equal(got, ref) and np.array_equal(run, rref)
+        else:
+            # recursive form: fill (digit tree) == direct chain bit for bit,
+            # both within 1e-12 of the counter form (test_halton.py:161-175)
+            assert np.array_equal(run, s.points_at(ridx).cpu().numpy())
+            assert np.abs(got - ref).max() <= 1e-12 and np.abs(run - rref).max() <= 1e-12
 
 
 def test_inv_normal(P, golden):
