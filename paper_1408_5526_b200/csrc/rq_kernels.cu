@@ -2220,6 +2220,7 @@ constexpr int BAR_PROD = 1, BAR_CONS = 2, BAR_FULL0 = 3, BAR_EMPTY0 = 5;  // FUL
 #ifndef RQ_WS_MINB
 #define RQ_WS_MINB 3
 #endif
+
 template <class G, class Mdl>
 __global__ void __launch_bounds__(2 * TILE, RQ_WS_MINB) k_paths_ws(PathArgs a) {
   extern __shared__ __align__(16) double z[];  // 2 x ZT_BYTES (+ model dyn)
