@@ -88,12 +88,33 @@ class DeviceSampler:
         return out
 
     # -- reference protocol ---------------------------------------------
+    # Sequential streams (MT19937, XORWOW, Kakutani) are positioned by
+    # walking them from their start, so a call at point `first` costs
+    # O(first); fill() reads ahead a block of up to READAHEAD_BYTES of points
+    # and serves consecutive fills from it (repeated small fills, e.g. the
+    # CLI's 8192-row blocks, are O(n) overall instead of O(n^2)).
+    READAHEAD_BYTES = 256 << 20
+    SEQUENTIAL = frozenset({"twister", "xorwow", "kakutani"})
+
     def fill(self, out) -> None:
         """Write the next ``len(out)`` points of the stream into ``out``."""
         n = int(out.shape[0])
-        pts = self.points(self._next, n)
+        if self.name in self.SEQUENTIAL:
+            pts = self._readahead(self._next, n)
+        else:
+            pts = self.points(self._next, n)
         self._next += n
         _store(out, pts)
+
+    def _readahead(self, first: int, n: int):
+        buf, b0 = getattr(self, "_ra", None), getattr(self, "_ra_first", 0)
+        if buf is None or first < b0 or first + n > b0 + buf.shape[0]:
+            rows = max(n, self.READAHEAD_BYTES // (8 * self.dim))
+            lim = int(_lib.lib().rq_index_limit(_lib.GEN_IDS[self.name]))
+            rows = max(n, min(rows, lim - first))
+            self._ra, self._ra_first = self.points(first, rows), first
+            buf, b0 = self._ra, first
+        return buf[first - b0:first - b0 + n]
 
     def at(self, indices):
         if not self.counter_based:

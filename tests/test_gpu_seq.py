@@ -80,6 +80,22 @@ def test_fill_sequence_matches_reference(P, golden, gen):
     assert np.array_equal(out[rows[sel]], ref[sel])
 
 
+@pytest.mark.parametrize("gen", ["twister", "xorwow", "kakutani"])
+def test_fill_readahead_refills(P, gen, monkeypatch):
+    """Consecutive fills of a sequential stream are served from a read-ahead
+    block (ADVICE r01: repeated fills re-walked the stream from its start);
+    a small block forces refills across its boundaries."""
+    from paper_1408_5526_b200.samplers import DeviceSampler
+
+    monkeypatch.setattr(DeviceSampler, "READAHEAD_BYTES", 8 * 5 * 1000)  # 1000-row blocks
+    s = DeviceSampler(gen, 5, SEED, 2)
+    out = np.empty((5000, 5))
+    for a in range(0, 5000, 777):
+        s.fill(out[a:a + 777])
+    ref = DeviceSampler(gen, 5, SEED, 2).points(0, 5000).cpu().numpy()
+    assert np.array_equal(out, ref)
+
+
 @pytest.mark.parametrize("gen", ["twister", "xorwow"])
 def test_word_streams_vs_oracle_many_segments(P, oracle, gen):
     """A long fill that spans many device segments (and jump/snapshot starts)."""
