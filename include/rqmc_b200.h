@@ -120,7 +120,9 @@ int rq_sampler_rasrap_tables(rq_sampler *s, int32_t rep_local, uint16_t *digits_
 /* The fused replication engine: for every replication of the sampler and
  * every N in grid (strictly increasing), theta[r][g] = np.sum(payoffs[:N])/N
  * (harness.py:291-315, with numpy's pairwise summation order).
- * theta_dev[rep_count][ngrid].  kernel_launches (nullable) += kernels run. */
+ * theta_dev[rep_count][ngrid].  kernel_launches (nullable) += kernels run.
+ * N <= min(2^40, rq_index_limit(generator)); marks above RQ_SEG_PATHS
+ * (env, default 2^31) run as pairwise-tree segments (same result). */
 int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, int32_t ngrid,
                 double *theta_dev, int32_t *kernel_launches, void *stream);
 

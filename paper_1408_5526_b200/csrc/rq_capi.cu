@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -863,8 +864,32 @@ static int check_grid(const int64_t *grid, int32_t ngrid) {
     if (grid[g] < 1) return fail(RQ_ERR_VALUE, "n_grid must be a nonempty list of positive sizes");
     if (g && grid[g] <= grid[g - 1]) return fail(RQ_ERR_VALUE, "n_grid must be strictly increasing");
   }
-  if (grid[ngrid - 1] > ((int64_t)1 << 32)) return fail(RQ_ERR_RANGE, "N exceeds 2^32 paths");
+  if (grid[ngrid - 1] > ((int64_t)1 << 40)) return fail(RQ_ERR_RANGE, "N exceeds 2^40 paths");
   return RQ_OK;
+}
+
+// numpy's pairwise summation of n values (numpy/_core/src/umath/
+// loops_utils.h.src: n > 128 splits at n2 = n/2 - (n/2 mod 8)), cut into its
+// subtrees of <= seg values: the leaves of the cut in order ...
+constexpr int64_t TILE_PATHS = 128;  // rq_kernels.cu TILE: segment payoff spans are tile-aligned
+
+static void seg_nodes(int64_t a, int64_t n, int64_t seg, std::vector<std::pair<int64_t, int64_t>> &out) {
+  if (n <= seg) {
+    out.emplace_back(a, n);
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  seg_nodes(a, n2, seg, out);
+  seg_nodes(a + n2, n - n2, seg, out);
+}
+// ... and the sum of their subtree sums in the same tree order.
+static double seg_combine(int64_t n, int64_t seg, const double *sums, size_t &k) {
+  if (n <= seg) return sums[k++];
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  const double l = seg_combine(n2, seg, sums, k);
+  return l + seg_combine(n - n2, seg, sums, k);
 }
 
 int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, int32_t ngrid,
@@ -872,55 +897,128 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
   if (!s) return fail(RQ_ERR_VALUE, "sampler is NULL");
   int rc = check_grid(grid_host, ngrid);
   if (rc) return rc;
+  if (grid_host[ngrid - 1] > rq_index_limit(s->t.gen))
+    return fail(RQ_ERR_RANGE, "N = %lld exceeds the generator's index range %lld",
+                (long long)grid_host[ngrid - 1], (long long)rq_index_limit(s->t.gen));
   cudaStream_t st = (cudaStream_t)stream;
   rq::ModelParams mp;
   DevMem tab;
   if ((rc = model_to_params(model, s->t.dim, mp, tab, st))) return rc;
-  const int64_t nmax = grid_host[ngrid - 1];
-  // replication batch: payoff buffer <= 1 GiB (2^27 paths), >= 1 replication
-  int64_t B = std::max<int64_t>(1, env_int("RQ_BATCH_PATHS", (int64_t)128 << 20) / nmax);
-  B = std::min<int64_t>(B, s->t.rep_count);
-  B = std::min<int64_t>(B, 65535);  // the reduction's grid.y
-  std::vector<HostPlan> hplans(ngrid);
-  std::vector<DevPlan> dplans(ngrid);
-  int32_t maxnodes = 1;
-  for (int g = 0; g < ngrid; g++) {
-    build_plan(grid_host[g], hplans[g]);
-    maxnodes = std::max(maxnodes, hplans[g].nnodes);
-    if ((rc = upload_plan(hplans[g], dplans[g], st))) return rc;
-  }
-  DevMem pay_m(st), scratch_m(st), tickets_m(st);
-  RQ_CUDA(pay_m.alloc(sizeof(double) * B * nmax));
-  RQ_CUDA(scratch_m.alloc(sizeof(double) * B * maxnodes));
-  RQ_CUDA(tickets_m.alloc(sizeof(unsigned) * B));
-  double *pay = pay_m.as<double>(), *scratch = scratch_m.as<double>();
-  unsigned *tickets = tickets_m.as<unsigned>();
-  RQ_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * B, st));
+  // Grid marks up to SEG paths share one payoff buffer per replication batch
+  // (prefixes of one pass); longer marks (counter-based generators) are
+  // evaluated in segments, each a subtree of numpy's pairwise tree, so no
+  // buffer exceeds SEG payoffs per replication.
+  const int64_t SEG = std::max<int64_t>(TILE_PATHS, env_int("RQ_SEG_PATHS", (int64_t)1 << 31));
+  const bool seq = rq::gen_sequential(s->t.gen);
+  int ns = 0;  // grid marks of the shared pass: grid[0 .. ns)
+  while (ns < ngrid && (seq || grid_host[ns] <= SEG)) ns++;
   int launched = 0;
-  SeqRun R;
-  if (rq::gen_sequential(s->t.gen) && (rc = seq_begin(s->t, mp, (int)B, 0, nmax, R, st)))
-    return rc;
-  for (int64_t r0 = 0; r0 < s->t.rep_count; r0 += B) {
-    int rn = (int)std::min<int64_t>(B, s->t.rep_count - r0);
-    cudaError_t e;
-    if (rq::gen_sequential(s->t.gen)) {
-      int blocks = 0;
-      if ((rc = seq_batch(s->t, (int)r0, rn, R, &blocks, &launched, st))) return rc;
-      KTimer kt(&g_stats.paths_ms, st);
-      e = rq::launch_paths_seq(s->t, mp, (int)r0, rn, nmax, R.q, blocks, pay, &launched, st);
-      stat_add(g_stats.paths_launches, (int64_t)1);
-    } else {
-      KTimer kt(&g_stats.paths_ms, st);
-      e = rq::launch_paths(s->t, mp, (int)r0, rn, nmax, pay, &launched, st);
-      stat_add(g_stats.paths_launches, (int64_t)1);
+  if (ns > 0) {
+    const int64_t nmax = grid_host[ns - 1];
+    // replication batch: payoff buffer <= 1 GiB (2^27 paths), >= 1 replication
+    int64_t B = std::max<int64_t>(1, env_int("RQ_BATCH_PATHS", (int64_t)128 << 20) / nmax);
+    B = std::min<int64_t>(B, s->t.rep_count);
+    B = std::min<int64_t>(B, 65535);  // the reduction's grid.y
+    std::vector<HostPlan> hplans(ns);
+    std::vector<DevPlan> dplans(ns);
+    int32_t maxnodes = 1;
+    for (int g = 0; g < ns; g++) {
+      build_plan(grid_host[g], hplans[g]);
+      maxnodes = std::max(maxnodes, hplans[g].nnodes);
+      if ((rc = upload_plan(hplans[g], dplans[g], st))) return rc;
     }
-    if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "path kernel: %s", cudaGetErrorString(e));
-    for (int g = 0; g < ngrid; g++) {
-      KTimer kt(&g_stats.reduce_ms, st);
-      e = rq::launch_reduce(dplans[g].p, pay, nmax, rn, theta_dev + r0 * ngrid + g, ngrid,
-                            scratch, tickets, st);
-      if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "reduce kernel: %s", cudaGetErrorString(e));
-      launched++;
+    DevMem pay_m(st), scratch_m(st), tickets_m(st);
+    RQ_CUDA(pay_m.alloc(sizeof(double) * B * nmax));
+    RQ_CUDA(scratch_m.alloc(sizeof(double) * B * maxnodes));
+    RQ_CUDA(tickets_m.alloc(sizeof(unsigned) * B));
+    double *pay = pay_m.as<double>(), *scratch = scratch_m.as<double>();
+    unsigned *tickets = tickets_m.as<unsigned>();
+    RQ_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * B, st));
+    SeqRun R;
+    if (seq && (rc = seq_begin(s->t, mp, (int)B, 0, nmax, R, st))) return rc;
+    for (int64_t r0 = 0; r0 < s->t.rep_count; r0 += B) {
+      int rn = (int)std::min<int64_t>(B, s->t.rep_count - r0);
+      cudaError_t e;
+      if (seq) {
+        int blocks = 0;
+        if ((rc = seq_batch(s->t, (int)r0, rn, R, &blocks, &launched, st))) return rc;
+        KTimer kt(&g_stats.paths_ms, st);
+        e = rq::launch_paths_seq(s->t, mp, (int)r0, rn, nmax, R.q, blocks, pay, &launched, st);
+        stat_add(g_stats.paths_launches, (int64_t)1);
+      } else {
+        KTimer kt(&g_stats.paths_ms, st);
+        e = rq::launch_paths(s->t, mp, (int)r0, rn, 0, nmax, pay, &launched, st);
+        stat_add(g_stats.paths_launches, (int64_t)1);
+      }
+      if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "path kernel: %s", cudaGetErrorString(e));
+      for (int g = 0; g < ns; g++) {
+        KTimer kt(&g_stats.reduce_ms, st);
+        e = rq::launch_reduce(dplans[g].p, pay, nmax, rn, theta_dev + r0 * ngrid + g, ngrid,
+                              scratch, tickets, st);
+        if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "reduce kernel: %s", cudaGetErrorString(e));
+        launched++;
+      }
+    }
+  }
+  if (ns < ngrid) {  // segmented marks, one replication at a time
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> nodes(ngrid);
+    std::map<int64_t, DevPlan> plans;  // pairwise plan per subtree length (a few distinct)
+    int32_t maxnodes = 1;
+    int64_t maxspan = 0;
+    size_t maxk = 0;
+    for (int g = ns; g < ngrid; g++) {
+      seg_nodes(0, grid_host[g], SEG, nodes[g]);
+      maxk = std::max(maxk, nodes[g].size());
+      for (auto &nd : nodes[g]) {
+        const int64_t a0 = nd.first / TILE_PATHS * TILE_PATHS;
+        maxspan = std::max(maxspan, (nd.first + nd.second + TILE_PATHS - 1) / TILE_PATHS * TILE_PATHS - a0);
+        if (!plans.count(nd.second)) {
+          HostPlan hp;
+          build_plan(nd.second, hp);
+          maxnodes = std::max(maxnodes, hp.nnodes);
+          if ((rc = upload_plan(hp, plans[nd.second], st))) return rc;
+          plans[nd.second].p.n = 1;  // the subtree's sum, not a mean
+        }
+      }
+    }
+    DevMem pay_m(st), scratch_m(st), tickets_m(st), sums_m(st);
+    RQ_CUDA(pay_m.alloc(sizeof(double) * maxspan));
+    RQ_CUDA(scratch_m.alloc(sizeof(double) * maxnodes));
+    RQ_CUDA(tickets_m.alloc(sizeof(unsigned)));
+    RQ_CUDA(sums_m.alloc(sizeof(double) * maxk));
+    RQ_CUDA(cudaMemsetAsync(tickets_m.p, 0, sizeof(unsigned), st));
+    double *pay = pay_m.as<double>(), *sums_dev = sums_m.as<double>();
+    std::vector<double> sums(maxk), theta_host(ngrid - ns);
+    for (int64_t r = 0; r < s->t.rep_count; r++) {
+      for (int g = ns; g < ngrid; g++) {
+        for (size_t k = 0; k < nodes[g].size(); k++) {
+          const int64_t a = nodes[g][k].first, len = nodes[g][k].second;
+          const int64_t a0 = a / TILE_PATHS * TILE_PATHS;  // tile-aligned payoff span
+          const int64_t a1 = (a + len + TILE_PATHS - 1) / TILE_PATHS * TILE_PATHS;
+          cudaError_t e;
+          {
+            KTimer kt(&g_stats.paths_ms, st);
+            e = rq::launch_paths(s->t, mp, (int)r, 1, a0, a1 - a0, pay, &launched, st);
+            stat_add(g_stats.paths_launches, (int64_t)1);
+          }
+          if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "path kernel: %s", cudaGetErrorString(e));
+          {
+            KTimer kt(&g_stats.reduce_ms, st);
+            e = rq::launch_reduce(plans[len].p, pay + (a - a0), a1 - a0, 1, sums_dev + k, 1,
+                                  scratch_m.as<double>(), tickets_m.as<unsigned>(), st);
+          }
+          if (e != cudaSuccess) return fail(RQ_ERR_CUDA, "reduce kernel: %s", cudaGetErrorString(e));
+          launched++;
+        }
+        RQ_CUDA(cudaMemcpyAsync(sums.data(), sums_dev, sizeof(double) * nodes[g].size(),
+                                cudaMemcpyDeviceToHost, st));
+        RQ_CUDA(cudaStreamSynchronize(st));
+        size_t k = 0;
+        theta_host[g - ns] = seg_combine(grid_host[g], SEG, sums.data(), k) / (double)grid_host[g];
+      }
+      RQ_CUDA(cudaMemcpyAsync(theta_dev + r * ngrid + ns, theta_host.data(),
+                              sizeof(double) * (ngrid - ns), cudaMemcpyHostToDevice, st));
+      RQ_CUDA(cudaStreamSynchronize(st));  // theta_host is reused
     }
   }
   if (kernel_launches) *kernel_launches += launched;

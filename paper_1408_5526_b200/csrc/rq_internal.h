@@ -133,7 +133,7 @@ cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32
 cudaError_t launch_points(const RepTables &t, int rep_local, int64_t first,
                           const int64_t *idx, int64_t count, double *out, cudaStream_t s);
 cudaError_t launch_paths(const RepTables &t, const ModelParams &mp, int rep_local0,
-                         int rep_n, int64_t nmax, double *payoffs, int *launched,
+                         int rep_n, int64_t p0, int64_t nmax, double *payoffs, int *launched,
                          cudaStream_t s);
 cudaError_t upload_xorwow_jumps(const uint32_t *cols, size_t words);
 cudaError_t upload_kakutani_tables(const double *thr, const double *b, int dims);

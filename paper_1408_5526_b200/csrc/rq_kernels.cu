@@ -2095,9 +2095,10 @@ struct PathArgs {
   RepTables t;
   ModelParams mp;
   int rep_local0, rep_n;
-  int64_t nmax;
+  int64_t p0;    // first path (a multiple of TILE; segments of long estimates)
+  int64_t nmax;  // paths p0 .. p0 + nmax - 1
   int64_t tiles_per_rep;
-  double *payoffs;  // [rep_n][nmax]
+  double *payoffs;  // [rep_n][nmax], path p0 + i at i
 };
 
 constexpr size_t ZT_BYTES = sizeof(double) * CHUNK * TILE;  // one uniform/normal tile
@@ -2172,7 +2173,7 @@ __global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathAr
   };
   Cursor cur{a.rep_local0 + lo / tpr, 0, lo % tpr};
   auto dc_of = [&](int c) { return gdims - c * CHUNK < CHUNK ? gdims - c * CHUNK : CHUNK; };
-  auto base_of = [&](const Cursor &q) { return (int64_t)q.tile * TILE; };
+  auto base_of = [&](const Cursor &q) { return a.p0 + (int64_t)q.tile * TILE; };
   for (int u = 0; u < nunit; u++) {
     const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
     const int64_t base = base_of(cur);
@@ -2186,9 +2187,8 @@ __global__ void __launch_bounds__(TILE, PathsMinB<G, Mdl>::value) k_paths(PathAr
           z, Dc, phs.tq[warp]);
     md.chunk(d0, Dc, z + threadIdx.x);
     if (d0 + Dc >= gdims) {
-      const int64_t path = base + threadIdx.x;
-      if (path < a.nmax)
-        a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.payoff();
+      const int64_t i = base - a.p0 + threadIdx.x;
+      if (i < a.nmax) a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + i] = md.payoff();
     }
     __syncthreads();
     advance(cur);
@@ -2265,7 +2265,7 @@ __global__ void __launch_bounds__(2 * TILE, RQ_WS_MINB) k_paths_ws(PathArgs a) {
       const int buf = u & 1;
       double *zb = z + buf * (CHUNK * TILE);
       const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
-      const int64_t base = (int64_t)cur.tile * TILE;
+      const int64_t base = a.p0 + (int64_t)cur.tile * TILE;
       if (u >= 2) {  // the consumers are done with zb
         if (buf) nbar_sync<BAR_EMPTY0 + 1, 2 * TILE>();
         else nbar_sync<BAR_EMPTY0, 2 * TILE>();
@@ -2291,15 +2291,14 @@ __global__ void __launch_bounds__(2 * TILE, RQ_WS_MINB) k_paths_ws(PathArgs a) {
       const int buf = u & 1;
       const double *zb = z + buf * (CHUNK * TILE);
       const int rl = cur.rl, d0 = cur.c * CHUNK, Dc = dc_of(cur.c);
-      const int64_t base = (int64_t)cur.tile * TILE;
+      const int64_t base = a.p0 + (int64_t)cur.tile * TILE;
       if (buf) nbar_sync<BAR_FULL0 + 1, 2 * TILE>();  // the producers filled zb
       else nbar_sync<BAR_FULL0, 2 * TILE>();
       if (d0 == 0) md.begin();
       md.chunk(d0, Dc, zb + t);
       if (d0 + Dc >= gdims) {
-        const int64_t path = base + t;
-        if (path < a.nmax)
-          a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + path] = md.payoff();
+        const int64_t i = base - a.p0 + t;
+        if (i < a.nmax) a.payoffs[(int64_t)(rl - a.rep_local0) * a.nmax + i] = md.payoff();
       }
       if (buf) nbar_arrive<BAR_EMPTY0 + 1, 2 * TILE>();
       else nbar_arrive<BAR_EMPTY0, 2 * TILE>();
@@ -2934,12 +2933,14 @@ static cudaError_t paths_dispatch(const PathArgs &a, int *launched, cudaStream_t
 }
 
 cudaError_t launch_paths(const RepTables &t, const ModelParams &mp, int rep_local0, int rep_n,
-                         int64_t nmax, double *payoffs, int *launched, cudaStream_t s) {
+                         int64_t p0, int64_t nmax, double *payoffs, int *launched,
+                         cudaStream_t s) {
   PathArgs a;
   a.t = t;
   a.mp = mp;
   a.rep_local0 = rep_local0;
   a.rep_n = rep_n;
+  a.p0 = p0;
   a.nmax = nmax;
   a.tiles_per_rep = (nmax + TILE - 1) / TILE;
   a.payoffs = payoffs;

@@ -204,3 +204,44 @@ def test_mbs_payoffs_high_variance(P, oracle, var):
     got = m.payoffs(u)
     assert np.all(np.isfinite(got))
     assert np.abs(got / ref - 1).max() <= 1e-12
+
+
+SEG_GENS = ["rasrap-recursive", "rasrap-counter", "philox", "sobol-gray", "sfc64"]
+
+
+@pytest.mark.parametrize("gen", SEG_GENS)
+def test_segmented_estimates_match(P, oracle, gen, monkeypatch):
+    """Grid marks longer than RQ_SEG_PATHS are evaluated in segments, each a
+    subtree of numpy's pairwise tree (harness.py:314), combined in tree
+    order: forcing tiny segments must reproduce the single-pass theta bit for
+    bit (x1 against the oracle, LIBOR against the unsegmented device run)."""
+    from paper_1408_5526_b200 import models as M
+
+    grid = (1000, 50_000, 100_003)
+    x1 = M.FirstCoordinateModel()
+    libor = _libor(5.0)
+    base_x1 = _gpu(gen, x1, 3, grid)
+    base_l = _gpu(gen, libor, 3, grid)
+    for seg in ("4096", "128"):
+        monkeypatch.setenv("RQ_SEG_PATHS", seg)
+        assert np.array_equal(_gpu(gen, x1, 3, grid), base_x1)
+        assert np.array_equal(_gpu(gen, libor, 3, grid), base_l)
+    monkeypatch.delenv("RQ_SEG_PATHS")
+    ref = oracle.run_replications(gen, x1, SEED, 1, 3, grid, threads=3,
+                                  sobol_v=_sobol_v(gen, x1.dim))
+    assert np.array_equal(base_x1, ref)
+
+
+def test_estimates_beyond_2_32_paths(P):
+    """N > 2^32 paths per replication (the reference sums any N): segmented
+    on the device; f = 1 is exact, f = x1 within 6 standard errors of 1/2,
+    and Sobol' (32-bit direction numbers) is refused."""
+    from paper_1408_5526_b200 import models as M
+
+    n = 2**32 + 1000
+    th = _gpu("philox", M.ConstantModel(), 2, (2**31 + 8, n))
+    assert np.array_equal(th, np.ones_like(th))
+    th = _gpu("philox", M.FirstCoordinateModel(), 2, (2**31 + 8, n))
+    assert np.all(np.abs(th - 0.5) < 6 * (1 / np.sqrt(12 * 2**31)))
+    with pytest.raises(ValueError):
+        _gpu("sobol-gray", M.FirstCoordinateModel(), 1, (n,))
