@@ -1049,6 +1049,9 @@ int rq_run_replications(int generator, const rq_model *model, uint64_t seed, int
   if (rep_count < 1) return fail(RQ_ERR_VALUE, "need at least one replication");
   int rc = check_grid(grid_host, ngrid);
   if (rc) return rc;
+  if (generator >= 0 && generator <= rq::GEN_LAST && grid_host[ngrid - 1] > rq_index_limit(generator))
+    return fail(RQ_ERR_RANGE, "N = %lld exceeds the generator's index range %lld",
+                (long long)grid_host[ngrid - 1], (long long)rq_index_limit(generator));
   // one non-blocking stream per device (a process may drive several GPUs)
   static std::mutex smu;
   static cudaStream_t streams[64] = {};

@@ -105,10 +105,14 @@ def test_validation_errors_before_device_work(lib):
     rc = lib.rq_run_replications(0, C.byref(m), 0, 1, 2, bad.ctypes.data_as(C.POINTER(C.c_int64)),
                                  2, theta.ctypes.data_as(C.POINTER(C.c_double)), None)
     assert rc == -1 and b"increasing" in lib.rq_last_error()
-    big = np.array([2**33], dtype=np.int64)
+    big = np.array([2**41], dtype=np.int64)  # beyond the 2^40 cap
     rc = lib.rq_run_replications(0, C.byref(m), 0, 1, 2, big.ctypes.data_as(C.POINTER(C.c_int64)),
                                  1, theta.ctypes.data_as(C.POINTER(C.c_double)), None)
     assert rc == -3
+    big = np.array([2**33], dtype=np.int64)  # beyond Sobol's 2^32 index range
+    rc = lib.rq_run_replications(3, C.byref(m), 0, 1, 2, big.ctypes.data_as(C.POINTER(C.c_int64)),
+                                 1, theta.ctypes.data_as(C.POINTER(C.c_double)), None)
+    assert rc == -3 and b"index range" in lib.rq_last_error()
 
 
 def test_error_codes_map_to_reference_exceptions():
