@@ -60,6 +60,9 @@
 #ifndef RQ_TAIL_CAND
 #define RQ_TAIL_CAND 1  // inverse-normal tail test on the high word (exact re-test in the queue)
 #endif
+#ifndef RQ_SW_TABLES
+#define RQ_SW_TABLES 1  // persistent Rasrap tile: sigma*w_0 / sigma*w_1 tables, two-level fast path
+#endif
 #ifndef RQ_WS
 #define RQ_WS 1  // warp-specialised path kernel (producer / consumer warpgroups)
 #endif
@@ -236,6 +239,12 @@ struct RasrapTilePersistShared : RasrapTileShared {
 // CHUNK dims)
 struct RasrapTilePersistSigShared : RasrapTilePersistShared {
   double sigd[SIGD_MAX];
+#if RQ_SW_TABLES
+  // sigma(a) * w_0 and sigma(a) * w_1 per dim (the products the tree forms
+  // at levels 0 and 1, same rounding): a two-level tile (J <= 2) needs no
+  // level pass -- every leaf adds its parent's and its own term directly
+  double sw0[SIGD_MAX], sw1[SIGD_MAX];
+#endif
 };
 struct RasrapDirectShared {
   uint16_t scr[MAX_CAP][TILE];  // per-thread digits (direct path)
@@ -546,8 +555,19 @@ struct GenRasrapRecTile {
     for (int k = 0, dd; (dd = dim_slot(warp, k, d0, Dc)) >= 0; k++) {
       const HaltonDim &h = c_hdim[d0 + dd];
       const int o = h.sig_off - off0;
-      if constexpr (SIGSM)
-        for (int a = lane; a < h.base; a += 32) R.sigd[o + a] = (double)gsig[h.sig_off + a];
+      if constexpr (SIGSM) {
+#if RQ_SW_TABLES
+        const double w0 = c_wts[h.sum_off], w1 = c_wts[h.sum_off + 1];
+#endif
+        for (int a = lane; a < h.base; a += 32) {
+          const double sv = (double)gsig[h.sig_off + a];
+          R.sigd[o + a] = sv;
+#if RQ_SW_TABLES
+          R.sw0[o + a] = dmul(sv, w0);
+          R.sw1[o + a] = dmul(sv, w1);
+#endif
+        }
+      }
       if (lane == 0) R.soff[dd] = o;
     }
     __syncwarp();
@@ -625,6 +645,30 @@ struct GenRasrapRecTile {
       // the init sum of a level above hB (node 0 is then n0's prefix): for a
       // persistent state P[j] = S_j(B) = init_sums[j] there (shared memory)
       auto init_at = [&](int j) { return persist ? pers_P(dd, j) : ini[j]; };
+#if RQ_SW_TABLES
+      if constexpr (SIGSM) {
+        if (J <= 2) {  // two-level tile: leaf = (S_J [+ sigma(b1 + par) w_1]) + sigma(a) w_0
+          const uint32_t sws = smem_addr(sh->sw0 + sh->soff[dd]);
+          const uint32_t sws1 = smem_addr(sh->sw1 + sh->soff[dd]) + 8u * (uint32_t)R.bd[dd][1];
+          const uint32_t b0 = R.bd[dd][0];
+          const double top = R.sJ[dd];
+          const double p1 = J == 2 && 1 > hB ? init_at(1) : 0.0;  // level-1 node 0 = n0's prefix
+#pragma unroll
+          for (int m = 0; m < TILE / 32; m++) {
+            const int k = lane + 32 * m;
+            const uint32_t x = b0 + (uint32_t)k;
+            const uint32_t par = __umulhi(x, m16);
+            const uint32_t a = x - par * p;
+            double vp = top;  // J == 1: every leaf's parent is the top node
+            if (J == 2) vp = par == 0 && 1 > hB ? p1 : dadd(top, lds_f64(sws1 + 8u * par));
+            double o = dadd(vp, lds_f64(sws + 8u * a));
+            if (0 > hB && k == 0) o = ini[0];
+            zt[dd * TILE + k] = o;
+          }
+          continue;
+        }
+      }
+#endif
       double *prev = ph->lev[warp][0], *next = ph->lev[warp][1];
       // Levels of <= 32 nodes live in registers, lane k holding node k, and
       // a child reads its parent with a shuffle (every level above 1 for
