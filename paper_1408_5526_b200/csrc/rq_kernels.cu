@@ -2900,8 +2900,10 @@ static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bo
   // only where it measured faster (the persistent Rasrap tile with LIBOR
   // S <= 20), 2: every eligible pair (experiments)
   constexpr bool ws_ok = !std::is_same<G, GenRasrapCounterTile>::value;
+  // (the xhash test integrand takes the same kernel, so its bit-exact theta
+  // pins the warp-specialised generator path the C2 headline runs)
   constexpr bool ws_pick = RQ_WS >= 2 || (std::is_same<G, GenRasrapRecTile<true>>::value &&
-                                          Mdl::SMALL_LIBOR);
+                                          (Mdl::SMALL_LIBOR || std::is_same<Mdl, ModelHash>::value));
   if constexpr (ws_ok && ws_pick) {
     size_t dyn = prep_dyn(k_paths_ws<G, Mdl>, 2 * ZT_BYTES + ModelDyn<Mdl>::bytes(a.mp.dim));
     int per_sm = 0;
