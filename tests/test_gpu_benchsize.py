@@ -245,3 +245,24 @@ def test_estimates_beyond_2_32_paths(P):
     assert np.all(np.abs(th - 0.5) < 6 * (1 / np.sqrt(12 * 2**31)))
     with pytest.raises(ValueError):
         _gpu("sobol-gray", M.FirstCoordinateModel(), 1, (n,))
+
+
+@pytest.mark.timeout(900)
+def test_sharded_device_pipeline_under_torchrun(P):
+    """The device pipeline under torchrun with 3 ranks (sharing the box's
+    GPU over gloo): a fixed M=37 split 13/12/12, theta gathered once --
+    bit-identical to one process (harness.py:349-358 worker-count invariance)."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "3", "--master-addr", "127.0.0.1",
+                        "--master-port", "29547", "tests/_torchrun_device.py"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    one = _gpu("rasrap-recursive", _libor(5.0), 37, (1000, 2**17))
+    assert d["world"] == 3 and np.array_equal(np.array(d["theta"]), one)
