@@ -111,3 +111,22 @@ def test_criterion_9_single_month_collapse():
     pv = m.payoffs(u)
     expected = m.config.payment / (1 + m.config.initial_rate)
     assert np.allclose(pv, expected, rtol=0, atol=1e-15)
+
+
+def test_report_timing_is_measured_per_mark():
+    """time_s per grid mark is the measured mean wall time per replication of
+    a call that stops at that mark (harness.py:300-313), so it grows with N;
+    efficiency = std x time_s (harness.py:364-385)."""
+    import paper_1408_5526_b200 as P
+    from paper_1408_5526_b200 import models as M
+
+    cfg = P.ExperimentConfig(model="libor", generator="rasrap-recursive",
+                             n_grid=(2**12, 2**16, 2**20), replications=64, seed=SEED)
+    rep = P.run_experiment(cfg, model=M.LiborModel(M.LiborConfig(maturity=5.0, accrual=0.25)))
+    t = [rep.row("rasrap-recursive", n).seconds for n in cfg.n_grid]
+    assert t[0] < t[2] and t[1] < t[2]
+    for n in cfg.n_grid:
+        r = rep.row("rasrap-recursive", n)
+        assert r.efficiency == r.std * r.seconds
+    with pytest.raises(ValueError):
+        P.run_experiment(cfg, timing="guess")
