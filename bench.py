@@ -209,7 +209,24 @@ def run_stream(args) -> dict:
     t = float(np.mean(ms))
     normals = npts * dim
     value = normals / (t * 1e-3)
-    return {
+    # end to end through the public API: randomisation setup, the stream,
+    # the sum read back to the host, every step
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h2 = C.c_void_p()
+        _lib.check(lib.rq_sampler_create(C.byref(h2), _lib.GEN_IDS[args.generator], dim, SEED, 0,
+                                         1, st))
+        _lib.check(lib.rq_stream_normals(h2, 0, npts, out.data_ptr(), None, st))
+        total = float(out.item())
+        lib.rq_sampler_destroy(h2)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e = {"value": normals / (float(np.mean(e2e_ms)) * 1e-3), "unit": "normals/s",
+           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
+           "api": "rq_sampler_create + rq_stream_normals (sum to host)"}
+    assert math.isfinite(total)
+    out = {
         "metric": "C4 normals/sec (fused inverse normal, s=360 stream)", "value": value,
         "unit": "normals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -220,7 +237,14 @@ def run_stream(args) -> dict:
                      "peak": peak / 1e12, "unit": "Tslot/s (36 slots/normal)",
                      "frac": value * NORMAL_SLOTS / peak},
         "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": args.steps * 2,  # stream kernel + pairwise sum of the block sums
     }
+    if not args.no_cpu_baseline:
+        ref = run_reference_stream(argparse.Namespace(generator=args.generator, steps=1,
+                                                      warmup=1))
+        out["cpu_baseline"] = ref["cpu_baseline"]
+    return out
 
 
 def workload_config(args) -> tuple:
@@ -517,10 +541,73 @@ def cpu_baseline(model, gen, M, N, theta_gpu) -> tuple[dict, dict]:
     return cb, par
 
 
+def cpu_stream_normals(gen: str, first: int, count: int, dim: int = 360) -> float:
+    """Config 4 on the host: the oracle's points first..first+count-1 of
+    replication 0 (the reference layouts) through the reference Phi^-1,
+    summed.  Returns the sum."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    idx = np.arange(first, first + count, dtype=np.int64)
+    if gen == "philox":
+        u = O.philox_words(O.derive_key(SEED, 3, 0), idx, dim) * 2.0**-32 + 2.0**-33
+    elif gen == "sfc64":
+        u = O.sfc64_uniforms(SEED, 0, idx, dim)
+    elif gen.startswith("sobol"):
+        from paper_1408_5526_b200.tables import sobol_directions
+
+        gv, sh = O.sobol_scramble(sobol_directions(dim), O.derive_key(SEED, 5, 0), 0)
+        ii = idx ^ (idx >> 1) if gen == "sobol-gray" else idx
+        u = O.sobol_counter_words(gv, sh, ii) * 2.0**-32
+    else:  # rasrap: the counter form at the indices (the recursive form equals it to 1e-12)
+        u = O.rasrap_counter(dim, O.derive_key(SEED, 4, 0), idx)
+    return float(O.inv_normal(u).sum())
+
+
+def run_reference_stream(args) -> dict:
+    """--impl reference --workload c4: the same normals stream on the host
+    cores (threads over point blocks; the ctypes calls release the GIL)."""
+    from oracle import oracle as O
+
+    cores = O.host_cores()
+    dim, pts = 360, 200_000  # bounded sample: 7.2e7 normals per step
+    blk = (pts + cores - 1) // cores
+
+    def step():
+        th = [threading.Thread(target=cpu_stream_normals,
+                               args=(args.generator, k * blk, min(blk, pts - k * blk), dim))
+              for k in range(cores) if k * blk < pts]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        return pts * dim / (time.perf_counter() - t0)
+
+    for _ in range(args.warmup):
+        cpu_stream_normals(args.generator, 0, 1000, dim)
+    v = float(statistics.median([step() for _ in range(args.steps)]))
+    return {
+        "metric": "C4 normals/sec (fused inverse normal, s=360 stream)", "impl": "reference",
+        "value": v, "unit": "normals/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": pts * dim / v * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seed 20120224, replication 0)",
+        "config": {"workload": WORKLOADS["c4"][5], "generator": args.generator, "dim": dim},
+        "cpu_baseline": {"value": v, "unit": "normals/s", "cores": cores, "kind": "port",
+                         "sample": f"{pts} points x {dim} dims per step, {args.generator} "
+                                   f"(oracle generator + reference Phi^-1), {cores} threads"},
+        "e2e": {"value": v, "unit": "normals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
 def run_reference(args) -> dict | None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    if args.workload == "c4":
+        return run_reference_stream(args)
     from oracle import oracle as O
 
     model, M, N, desc, cfg = workload_config(args)

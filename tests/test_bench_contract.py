@@ -49,3 +49,16 @@ def test_reference_arm_under_torchrun_one_line():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+@pytest.mark.timeout(600)
+def test_reference_arm_config4_stream():
+    """--workload c4 --impl reference: the oracle's generator and the
+    reference inverse normal on the host cores, one JSON line in normals/s."""
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "c4",
+                        "--generator", "philox", "--steps", "1", "--warmup", "1"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["impl"] == "reference" and d["unit"] == "normals/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["config"]["generator"] == "philox"
