@@ -662,7 +662,7 @@ def main():
     ap.add_argument("--generator", default="rasrap-recursive")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reps", type=int, default=0,
-                    help="override M (replications per GPU) for quick sub-runs")
+                    help="override M (total replications, split over the ranks; for c4 the point count) for quick sub-runs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
