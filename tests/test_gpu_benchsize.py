@@ -73,7 +73,7 @@ C2_IDS = np.r_[1:9, 1017:1025]
 
 
 @pytest.mark.parametrize("gen", ["rasrap-recursive", "rasrap-counter", "philox", "sobol-gray",
-                                 "sfc64"])
+                                 "sobol-counter", "sfc64", "twister", "xorwow", "kakutani"])
 def test_c2_theta_at_bench_size(P, oracle, gen):
     """Config 2: LIBOR S=20, M=1024 x N=2^20 on the GPU (8 payoff batches of
     128 replications), ids 1-8 and 1017-1024 vs the oracle."""
@@ -95,21 +95,23 @@ def test_c2_prefix_grid_at_bench_size(P, oracle):
     assert np.abs(got[ids - 1] / ref - 1).max() <= THETA_RTOL
 
 
-def test_c3_mbs_theta_at_bench_size(P, oracle):
-    """Config 3: MBS 360 months, rasrap-recursive, M=256 x N=10^6 (two
-    payoff batches), ids 1-4 and 253-256 vs the oracle."""
+@pytest.mark.parametrize("gen", ["rasrap-recursive", "philox", "sobol-gray", "xorwow"])
+def test_c3_mbs_theta_at_bench_size(P, oracle, gen):
+    """Config 3: MBS 360 months, M=256 x N=10^6 (two payoff batches), ids
+    1-4 and 253-256 vs the oracle (Rasrap is the config's generator; the
+    others are the reference's MBS acceptance set)."""
     from paper_1408_5526_b200 import models as M
 
     model = M.MbsModel()
     grid = (10**6,)
-    got = _gpu("rasrap-recursive", model, 256, grid)
+    got = _gpu(gen, model, 256, grid)
     ids = np.r_[1:5, 253:257]
-    ref = _oracle_ids(oracle, "rasrap-recursive", model, ids, grid)
+    ref = _oracle_ids(oracle, gen, model, ids, grid)
     err = np.abs(got[ids - 1] / ref - 1).max()
-    assert err <= THETA_RTOL, err
+    assert err <= THETA_RTOL, (gen, err)
 
 
-@pytest.mark.parametrize("gen", ["rasrap-recursive", "philox"])
+@pytest.mark.parametrize("gen", ["rasrap-recursive", "philox", "sobol-gray"])
 def test_c5_theta_at_bench_size(P, oracle, gen):
     """Config 5: LIBOR S=80 at N=2^20 (the first 256 of its 8192
     replications: two payoff batches), ids 1-4 and 253-256 vs the oracle."""
