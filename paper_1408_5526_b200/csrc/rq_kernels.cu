@@ -60,6 +60,9 @@
 #ifndef RQ_TAIL_CAND
 #define RQ_TAIL_CAND 1  // inverse-normal tail test on the high word (exact re-test in the queue)
 #endif
+#ifndef RQ_G2_FAST
+#define RQ_G2_FAST 1  // global-sigma Rasrap tiles: level-pass-free path for J == 1 / small J == 2
+#endif
 #ifndef RQ_SW_TABLES
 #define RQ_SW_TABLES 1  // persistent Rasrap tile: sigma*w_0 / sigma*w_1 tables, two-level fast path
 #endif
@@ -662,6 +665,36 @@ struct GenRasrapRecTile {
             double vp = top;  // J == 1: every leaf's parent is the top node
             if (J == 2) vp = par == 0 && 1 > hB ? p1 : dadd(top, lds_f64(sws1 + 8u * par));
             double o = dadd(vp, lds_f64(sws + 8u * a));
+            if (0 > hB && k == 0) o = ini[0];
+            zt[dd * TILE + k] = o;
+          }
+          continue;
+        }
+      }
+#endif
+#if RQ_G2_FAST
+      if constexpr (!SIGSM) {
+        // sigma in global memory (large bases): a tile whose top node is at
+        // level 1, or at level 2 above <= 2 level-1 nodes, needs no level
+        // pass and no shuffles -- the (<= 2) parents are formed per lane
+        if (J == 1 || (J == 2 && R.nn[dd][1] <= 2)) {
+          const uint32_t b0 = R.bd[dd][0];
+          const double w0 = cw ? c_wts[h.sum_off] : w[0];
+          const double top = R.sJ[dd];
+          double v0 = top, v1 = top;
+          if (J == 2) {
+            const uint32_t b1 = R.bd[dd][1];
+            const double w1 = cw ? c_wts[h.sum_off + 1] : w[1];
+            v0 = 1 > hB ? init_at(1) : dadd(top, dmul(u16d(sg[b1]), w1));
+            v1 = dadd(top, dmul(u16d(sg[b1 + 1 < p ? b1 + 1 : b1]), w1));
+          }
+#pragma unroll
+          for (int m = 0; m < TILE / 32; m++) {
+            const int k = lane + 32 * m;
+            const uint32_t x = b0 + (uint32_t)k;
+            const uint32_t par = __umulhi(x, m16);
+            const uint32_t a = x - par * p;
+            double o = dadd(par ? v1 : v0, dmul(u16d(sg[a]), w0));
             if (0 > hB && k == 0) o = ini[0];
             zt[dd * TILE + k] = o;
           }
