@@ -64,7 +64,8 @@ enum rq_model_kind {
 
 /* Model description = the arguments of the reference's payoff kernels
  * (_libor_payoffs models.py:271, _mbs_payoffs models.py:430).
- * LIBOR: dim = steps (10, 20, 40 or 80), delta = accrual, sigma, strike,
+ * LIBOR: dim = steps (1..6542; 10/20/40/80 register-resident, <= 160 in
+ *        shared memory, longer in global memory), delta = accrual, sigma, strike,
  *        front_factor = 1/(1 + delta*L_0(0)), table = l0[dim] (HOST).
  * MBS:   dim = months, i0..payment as MbsConfig, table = ck[dim] (HOST).
  * X1 / CONST1 / XHASH: dim only. */
@@ -87,7 +88,9 @@ int rq_abi_version(void);
 /* make_sampler(name, dim, seed, replication) for a range of replications
  * (harness.py:99-125; rasrap_config halton.py:345-360; random_scramble
  * sobol.py:259-270).  The randomisation is generated ON THE DEVICE (numpy
- * SeedSequence/PCG64 restated), bit-identical to the reference. */
+ * SeedSequence/PCG64 restated), bit-identical to the reference.
+ * Dimensions: Rasrap and Kakutani 1..6542 (the first 6542 primes, every base
+ * below 2^16), Sobol' 1..421 (the direction table), the PRNGs any. */
 int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
                       int64_t rep_first, int32_t rep_count, void *stream);
 void rq_sampler_destroy(rq_sampler *s);

@@ -229,14 +229,25 @@ def _primes_py(n: int):
     return out
 
 
-def _set_kakutani_tables(L):
-    thr, b = kakutani_tables(512)
+_KK_SET = [0]
+
+
+def _set_kakutani_tables(L, dims: int = 512):
+    thr, b = kakutani_tables(dims)
     L.orc_kakutani_set_tables(_p(thr, C.c_double), _p(b, C.c_double), thr.shape[0])
+    _KK_SET[0] = dims
+
+
+def _ensure_kakutani(dim: int):
+    """Bracket tables of at least `dim` dims in the C oracle (grown in 512s)."""
+    if dim > _KK_SET[0]:
+        _set_kakutani_tables(lib(), (dim + 511) // 512 * 512)
 
 
 def kakutani_points(dim: int, key: int, count: int) -> np.ndarray:
     """KakutaniSampler(dim, key).fill of `count` rows (halton.py:521-542)."""
     out = np.empty((count, dim))
+    _ensure_kakutani(dim)
     if lib().orc_kakutani_points(dim, key & 0xFFFFFFFFFFFFFFFF, count, _p(out, C.c_double)):
         raise ValueError("kakutani orbit left the 64-entry bracket tables")
     return out
@@ -330,6 +341,8 @@ def run_replications(generator: str, model, seed: int, first: int, count: int, g
     if sobol_v is None:
         sobol_v = np.zeros((1, 32), dtype=np.uint32)
     sobol_v = np.ascontiguousarray(sobol_v, dtype=np.uint32)
+    if generator == "kakutani":
+        _ensure_kakutani(dim)
     rc = lib().orc_run_replications(GEN_IDS[generator], mid, dim, _p(params, C.c_double), seed,
                                     first, count, _p(grid, C.c_int64), grid.size,
                                     _p(sobol_v, C.c_uint32), threads, _p(theta, C.c_double))

@@ -289,34 +289,42 @@ void kakutani_tables(int p, double *thr, double *b) {
     }
   }
 }
-const std::vector<double> &kakutani_host_tables() {  // [MAX_DIM][2][KK_TAB]
-  static std::vector<double> T;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    const HostTables &H = host_tables();
-    T.resize((size_t)rq::MAX_DIM * 2 * rq::KK_TAB);
-    for (int d = 0; d < rq::MAX_DIM; d++)
-      kakutani_tables(H.dims[d].base, &T[(size_t)d * 2 * rq::KK_TAB],
-                      &T[(size_t)d * 2 * rq::KK_TAB + rq::KK_TAB]);
-  });
-  return T;
+// Kakutani bracket tables, [dim][2][KK_TAB], computed on first use of a
+// dim range (big-integer powers: ~1.3 ms per dim, 8.5 s for all 6542)
+std::mutex g_kk_mu;
+std::vector<double> g_kk_T;
+int g_kk_n = 0;
+void kakutani_grow(int n) {  // caller holds g_kk_mu
+  if (n <= g_kk_n) return;
+  n = std::min(rq::MAX_DIM, (n + 511) / 512 * 512);
+  const HostTables &H = host_tables();
+  g_kk_T.resize((size_t)n * 2 * rq::KK_TAB);
+  for (int d = g_kk_n; d < n; d++)
+    kakutani_tables(H.dims[d].base, &g_kk_T[(size_t)d * 2 * rq::KK_TAB],
+                    &g_kk_T[(size_t)d * 2 * rq::KK_TAB + rq::KK_TAB]);
+  g_kk_n = n;
 }
-int ensure_kakutani_tables() {
-  static std::mutex mu;
-  static std::vector<int> done;
+// device copies of dims [0, n) on the current device
+int ensure_kakutani_tables(int n) {
+  static std::vector<std::pair<int, int>> done;  // (device, dims uploaded)
   int dev = 0;
   RQ_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lk(mu);
-  if (std::find(done.begin(), done.end(), dev) != done.end()) return RQ_OK;
-  const std::vector<double> &T = kakutani_host_tables();
-  std::vector<double> thr((size_t)rq::MAX_DIM * rq::KK_TAB), b(thr.size());
-  for (int d = 0; d < rq::MAX_DIM; d++)
+  std::lock_guard<std::mutex> lk(g_kk_mu);
+  for (auto &e : done)
+    if (e.first == dev && e.second >= n) return RQ_OK;
+  kakutani_grow(n);
+  const int m = g_kk_n;
+  std::vector<double> thr((size_t)m * rq::KK_TAB), b(thr.size());
+  for (int d = 0; d < m; d++)
     for (int k = 0; k < rq::KK_TAB; k++) {
-      thr[(size_t)d * rq::KK_TAB + k] = T[(size_t)d * 2 * rq::KK_TAB + k];
-      b[(size_t)d * rq::KK_TAB + k] = T[(size_t)d * 2 * rq::KK_TAB + rq::KK_TAB + k];
+      thr[(size_t)d * rq::KK_TAB + k] = g_kk_T[(size_t)d * 2 * rq::KK_TAB + k];
+      b[(size_t)d * rq::KK_TAB + k] = g_kk_T[(size_t)d * 2 * rq::KK_TAB + rq::KK_TAB + k];
     }
-  RQ_CUDA(rq::upload_kakutani_tables(thr.data(), b.data(), rq::MAX_DIM));
-  done.push_back(dev);
+  RQ_CUDA(rq::upload_kakutani_tables(thr.data(), b.data(), m));
+  bool found = false;
+  for (auto &e : done)
+    if (e.first == dev) e.second = m, found = true;
+  if (!found) done.emplace_back(dev, m);
   return RQ_OK;
 }
 
@@ -522,7 +530,9 @@ int rq_halton_divide(int d, uint64_t x, uint64_t *q64, uint32_t *q32) {
 
 int rq_kakutani_tables(int dim, double *thr_host, double *b_host) {
   if (dim < 1 || dim > rq::MAX_DIM) return fail(RQ_ERR_VALUE, "dim %d outside 1..%d", dim, rq::MAX_DIM);
-  const std::vector<double> &T = kakutani_host_tables();
+  std::lock_guard<std::mutex> lk(g_kk_mu);
+  kakutani_grow(dim);
+  const std::vector<double> &T = g_kk_T;
   for (int d = 0; d < dim; d++)
     for (int k = 0; k < rq::KK_TAB; k++) {
       if (thr_host) thr_host[(size_t)d * rq::KK_TAB + k] = T[(size_t)d * 2 * rq::KK_TAB + k];
@@ -640,7 +650,7 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
       delete S;
       return fail(RQ_ERR_VALUE, "kakutani dimension %d exceeds %d", dim, rq::MAX_DIM);
     }
-    if ((rc = ensure_kakutani_tables())) {
+    if ((rc = ensure_kakutani_tables(dim))) {
       delete S;
       return rc;
     }
@@ -708,7 +718,9 @@ static int seq_begin(const rq::RepTables &t, const rq::ModelParams &mp, int B, i
                                       (int64_t)per_rep / B * B);
   G = std::min<int64_t>(G, t.rep_count);
   R.grp_cap = G;
-  size_t b_scr = (mt ? sizeof(uint32_t) : sizeof(double)) * (size_t)R.ctas * t.dim * 128;
+  // per CTA: [dim][TILE] words (Kakutani: doubles, then the orbit state xs[dim])
+  size_t b_scr = mt ? sizeof(uint32_t) * (size_t)R.ctas * t.dim * rq::TILE_PATHS
+                    : sizeof(double) * (size_t)R.ctas * t.dim * (rq::TILE_PATHS + 1);
   RQ_CUDA(cudaMallocAsync(&R.mem, per_rep * G + b_scr, s));
   R.stream = s;
   R.snap = (uint32_t *)R.mem;
@@ -823,8 +835,8 @@ static int model_to_params(const rq_model *m, int dim, rq::ModelParams &mp, DevM
   if (m->kind < 0 || m->kind == rq::MODEL_POINTS || m->kind > rq::MODEL_XHASH)
     return fail(RQ_ERR_VALUE, "unknown model kind %d", m->kind);
   if (m->dim != dim) return fail(RQ_ERR_VALUE, "model dim %d != sampler dim %d", m->dim, dim);
-  if (m->kind == rq::MODEL_LIBOR && (m->dim < 1 || m->dim > rq::LIBOR_DYN_MAX))
-    return fail(RQ_ERR_VALUE, "LIBOR steps %d outside 1..%d", m->dim, rq::LIBOR_DYN_MAX);
+  if (m->kind == rq::MODEL_LIBOR && (m->dim < 1 || m->dim > rq::LIBOR_MAX))
+    return fail(RQ_ERR_VALUE, "LIBOR steps %d outside 1..%d", m->dim, rq::LIBOR_MAX);
   mp.kind = m->kind;
   mp.dim = m->dim;
   mp.delta = m->delta;
@@ -871,7 +883,7 @@ static int check_grid(const int64_t *grid, int32_t ngrid) {
 // numpy's pairwise summation of n values (numpy/_core/src/umath/
 // loops_utils.h.src: n > 128 splits at n2 = n/2 - (n/2 mod 8)), cut into its
 // subtrees of <= seg values: the leaves of the cut in order ...
-constexpr int64_t TILE_PATHS = 128;  // rq_kernels.cu TILE: segment payoff spans are tile-aligned
+using rq::TILE_PATHS;  // segment payoff spans are tile-aligned
 
 static void seg_nodes(int64_t a, int64_t n, int64_t seg, std::vector<std::pair<int64_t, int64_t>> &out) {
   if (n <= seg) {
@@ -901,7 +913,7 @@ int rq_estimate(rq_sampler *s, const rq_model *model, const int64_t *grid_host, 
     return fail(RQ_ERR_RANGE, "N = %lld exceeds the generator's index range %lld",
                 (long long)grid_host[ngrid - 1], (long long)rq_index_limit(s->t.gen));
   cudaStream_t st = (cudaStream_t)stream;
-  rq::ModelParams mp;
+  rq::ModelParams mp{};
   DevMem tab;
   if ((rc = model_to_params(model, s->t.dim, mp, tab, st))) return rc;
   // Grid marks up to SEG paths share one payoff buffer per replication batch
@@ -1099,7 +1111,7 @@ int rq_model_payoffs(const rq_model *model, const double *u_dev, int64_t npaths,
                      double *out_dev, void *stream) {
   if (!model) return fail(RQ_ERR_VALUE, "model is NULL");
   cudaStream_t st = (cudaStream_t)stream;
-  rq::ModelParams mp;
+  rq::ModelParams mp{};
   DevMem tab;
   int rc = model_to_params(model, model->dim, mp, tab, st);
   if (rc) return rc;

@@ -6,11 +6,20 @@
 
 namespace rq {
 
-constexpr int MAX_DIM = 512;    // Halton/Rasrap dimensions with universal tables
+// Halton/Rasrap/Kakutani dimensions: the first 6542 primes, i.e. every base
+// below 2^16 (digits and sigma entries are uint16; the reference takes any
+// count, halton.py:40-56, but its packed sigma table, halton.py:443-448, is
+// dim x max(base) int64 = 3.4 GB per sampler here).  The HaltonDim entries
+// of the first CONST_DIMS dims are in the constant bank, the rest in global
+// memory (see hdim in rq_kernels.cu).
+constexpr int MAX_DIM = 6542;
+constexpr int CONST_DIMS = 512;
 constexpr int MAX_CAP = 40;     // K + 8 for base 2 (largest digit window)
 constexpr int SOBOL_BITS = 32;  // sobol.py:30
+constexpr int TILE_PATHS = 128;  // paths per CTA tile (rq_kernels.cu TILE)
 constexpr int CHUNK_DIMS = 20;  // dimensions per generator chunk in the fused kernels
-constexpr int LIBOR_DYN_MAX = 160;  // LIBOR steps of the generic (shared-memory) model
+constexpr int LIBOR_DYN_MAX = 160;  // LIBOR steps of the generic shared-memory model
+constexpr int LIBOR_MAX = MAX_DIM;  // longer: forward rates in global memory (ModelLiborBig)
 constexpr int MBS_EXP_TERMS = 10;  // k0 exp(sigma_xi z) polynomial: z^0 .. z^9
 
 enum Gen : int {
@@ -110,6 +119,9 @@ struct ModelParams {
   // for |z| <= exp_zlim = 0.1 / sigma_xi)
   double ecoef[MBS_EXP_TERMS];
   double exp_zlim;
+  // LIBOR S > LIBOR_DYN_MAX: per-CTA forward-rate state [block][S][TILE]
+  // (allocated by the launcher, stream-ordered)
+  double *lstate;
 };
 
 // numpy pairwise-sum plan for one N (see rq_capi.cu build_plan).

@@ -75,26 +75,42 @@
 
 namespace rq {
 
-constexpr int TILE = 128;          // paths per CTA tile = threads per CTA
+constexpr int TILE = TILE_PATHS;   // paths per CTA tile = threads per CTA
 constexpr int CHUNK = CHUNK_DIMS;  // dimensions per unit (multiple of 4 for Philox)
 constexpr int WARPS = TILE / 32;
 constexpr double TWO_M32 = 2.3283064365386963e-10;  // 2^-32
 constexpr double TWO_M33 = 1.1641532182693481e-10;  // 2^-33
 constexpr double TWO_M53 = 1.1102230246251565e-16;  // 2^-53
 
-__constant__ HaltonDim c_hdim[MAX_DIM];
+__constant__ HaltonDim c_hdim[CONST_DIMS];
+__device__ HaltonDim g_hdim[MAX_DIM];  // every dim (those >= CONST_DIMS are read from here)
+// Dim d's constants: warp-uniform constant-bank reads below CONST_DIMS, L1-
+// cached global reads above.  The tile generators take WIDE (samplers of more
+// than CONST_DIMS dims, dispatched on the host) as a template parameter, so
+// the kernels of every benchmark configuration read c_hdim with no test;
+// hdim() serves the once-per-point paths (setup, at()).
+template <bool WIDE>
+__device__ __forceinline__ HaltonDim hdim_t(int d) {
+  if constexpr (WIDE) return g_hdim[d];
+  else return c_hdim[d];
+}
+__device__ __forceinline__ HaltonDim hdim(int d) {
+  return d < CONST_DIMS ? c_hdim[d] : g_hdim[d];
+}
 constexpr int CWTS = 1280;  // binpow weights of the first dims, in the constant bank
 static_assert(CHUNK_DIMS <= 40, "persistent Rasrap tiles assume their weights fit c_wts");
 static_assert(CHUNK_DIMS <= 20, "persistent Rasrap tiles stage sigma of <= 20 dims (639 entries)");
 __constant__ double c_wts[CWTS];
-constexpr int WTS_CAP = 16384;
+constexpr int WTS_CAP = 81920;  // sum over MAX_DIM dims of cap + 1 (78,909)
 __device__ double g_wts[WTS_CAP];     // binpow(inv_p, j+1): numba `x ** int` (halton.py:409)
 __device__ double g_cscale[WTS_CAP];  // counter-form scale chain (halton.py:436)
 
 cudaError_t upload_halton_dims(const HaltonDim *dims, int n, const double *wts,
                                const double *cscale, int nw) {
   if (n > MAX_DIM || nw > WTS_CAP) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemcpyToSymbol(c_hdim, dims, sizeof(HaltonDim) * n);
+  cudaError_t e = cudaMemcpyToSymbol(c_hdim, dims, sizeof(HaltonDim) * (n < CONST_DIMS ? n : CONST_DIMS));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyToSymbol(g_hdim, dims, sizeof(HaltonDim) * n);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyToSymbol(g_wts, wts, sizeof(double) * nw);
   if (e != cudaSuccess) return e;
@@ -137,7 +153,7 @@ __global__ void k_rasrap_setup(RepTables t, uint16_t *sigma, uint16_t *digits, d
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)t.rep_count * t.dim) return;
   int rl = (int)(gid / t.dim), d = (int)(gid % t.dim);
-  const HaltonDim h = c_hdim[d];
+  const HaltonDim h = hdim(d);
   uint64_t m = (uint64_t)(t.rep_first + rl);
   uint64_t key = derive_key3(t.seed, 4, m);  // harness.py:113, family "rasrap"
   Pcg64 g;
@@ -307,7 +323,7 @@ __device__ __forceinline__ void give_phase(G &g, PhaseShared &p) {
 // 2^40) for i < RQ_RASRAP_INDEX_MAX (2^39, checked by the C ABI).
 __device__ double rasrap_rec_direct(const RepTables &t, int rl, int d, uint64_t i,
                                     uint16_t *scr) {
-  const HaltonDim &h = c_hdim[d];
+  const HaltonDim h = hdim(d);
   const uint16_t *d0 = t.digits + (int64_t)rl * t.dig_stride + h.dig_off;
   const uint16_t *sg = t.sigma + (int64_t)rl * t.sig_stride + h.sig_off;
   const double *sums = t.sums + (int64_t)rl * t.sum_stride + h.sum_off;
@@ -361,8 +377,9 @@ struct GenRasrapRecDirect {
 // That is ~TILE * p/(p-1) node updates per tile and dim instead of
 // TILE * log_p(n) for independent per-point chains, with the same
 // operations in the same order as the reference (bit-identical).
-template <bool PERSIST, bool SIGSM = PERSIST>
+template <bool PERSIST, bool SIGSM = PERSIST, bool WIDE = false>
 struct GenRasrapRecTile {
+  static_assert(!(SIGSM && WIDE), "shared-memory sigma tiles have <= CHUNK dims");
   using Shared = typename std::conditional<
       PERSIST,
       typename std::conditional<SIGSM, RasrapTilePersistSigShared, RasrapTilePersistShared>::type,
@@ -379,6 +396,7 @@ struct GenRasrapRecTile {
   // of any dims over consecutive tiles, sigma read from global memory.
   static constexpr bool persist = PERSIST;
   static constexpr bool sig_smem = SIGSM;
+  __device__ __forceinline__ static HaltonDim hd(int d) { return hdim_t<WIDE>(d); }
   __device__ void setup(const RepTables &t_, Shared &s, int = 0) {
     t = &t_;
     sh = &s;
@@ -389,7 +407,7 @@ struct GenRasrapRecTile {
   // init_sums[hB+1]); used for a CTA's first tile of a replication.
   __device__ void state_full(int rl, uint64_t base, int d, int dd) {
     Shared &R = *sh;
-    const HaltonDim &h = c_hdim[d];
+    const HaltonDim h = hd(d);
     const uint32_t p = (uint32_t)h.base;
     const uint16_t *n0d = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
     const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
@@ -427,7 +445,7 @@ struct GenRasrapRecTile {
   // digit (>= h.tdig: the top digit of TILE changes or carries out).
   __device__ int digits_advance(int d, int dd) {
     Shared &R = *sh;
-    const HaltonDim &h = c_hdim[d];
+    const HaltonDim h = hd(d);
     const uint32_t p = (uint32_t)h.base;
     uint32_t r = TILE, carry = 0;
     int j = 0, jmax = -1;
@@ -453,7 +471,7 @@ struct GenRasrapRecTile {
   // at kmin = min(J, tdig + 1) instead of 0; P[k < kmin] go stale unused.
   __device__ void rechain(int rl, int d, int dd, int jmax, int kmin) {
     Shared &R = *sh;
-    const HaltonDim &h = c_hdim[d];
+    const HaltonDim h = hd(d);
     const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
     const double *w = g_wts + h.sum_off;
     const int hB = R.hB[dd];
@@ -478,7 +496,7 @@ struct GenRasrapRecTile {
   // per-dim tile state (one lane per dim): digits of B, hB, level sizes, S_J
   __device__ void prepare_dim(int rl, uint64_t base, int d, int dd) {
     RasrapTileShared &R = *sh;
-    const HaltonDim &h = c_hdim[d];
+    const HaltonDim h = hd(d);
     if (!persist) {  // stateless: digits up to the top level, S_J by one chain
       prepare_stateless(rl, base, d, dd);
       return;
@@ -505,7 +523,7 @@ struct GenRasrapRecTile {
   }
   __device__ void prepare_stateless(int rl, uint64_t base, int d, int dd) {
     RasrapTileShared &R = *sh;
-    const HaltonDim &h = c_hdim[d];
+    const HaltonDim h = hd(d);
     const uint32_t p = (uint32_t)h.base;
     const uint16_t *n0d = t->digits + (int64_t)rl * t->dig_stride + h.dig_off;
     const double *ini = t->sums + (int64_t)rl * t->sum_stride + h.sum_off;
@@ -553,10 +571,10 @@ struct GenRasrapRecTile {
     Shared &R = *sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint16_t *gsig = t->sigma + (int64_t)rl * t->sig_stride;
-    const int off0 = c_hdim[d0].sig_off;
+    const int off0 = hd(d0).sig_off;
 #pragma unroll 1
     for (int k = 0, dd; (dd = dim_slot(warp, k, d0, Dc)) >= 0; k++) {
-      const HaltonDim &h = c_hdim[d0 + dd];
+      const HaltonDim h = hd(d0 + dd);
       const int o = h.sig_off - off0;
       if constexpr (SIGSM) {
 #if RQ_SW_TABLES
@@ -632,7 +650,7 @@ struct GenRasrapRecTile {
         base2_points(rl, base, zt + dd * TILE);
         continue;
       }
-      const HaltonDim &h = c_hdim[d0 + dd];
+      const HaltonDim h = hd(d0 + dd);
       const uint32_t p = (uint32_t)h.base, m16 = h.m16;
       const uint16_t *sg = gsig + h.sig_off;
       // sigma of the dim staged as doubles: one 32-bit shared address, so the
@@ -788,7 +806,7 @@ struct GenRasrapCounter {
     const uint16_t *sig = t->sigma + (int64_t)rl * t->sig_stride;
 #pragma unroll 1
     for (int dd = 0; dd < Dc; dd++) {
-      const HaltonDim &h = c_hdim[d0 + dd];
+      const HaltonDim h = hdim(d0 + dd);
       const uint16_t *n0d = dig + h.dig_off;
       const uint16_t *sg = sig + h.sig_off;
       const double *cs = g_cscale + h.sum_off;
@@ -819,6 +837,7 @@ struct GenRasrapCounter {
 // formed once per tile and dim and then added in order: bit-identical, with
 // L instead of max(K, #digits) digit extractions per point.
 constexpr int CT_MAXT = 40;  // high terms per variant (digits of n >> L, n < 2^46)
+template <bool WIDE = false>
 struct GenRasrapCounterTile {
   static constexpr int MAXB = 4;
   struct Shared {
@@ -833,7 +852,7 @@ struct GenRasrapCounterTile {
     sh = &s;
   }
   __device__ void prepare(int rl, uint64_t base, int d, int dd) {  // one lane per dim
-    const HaltonDim &h = c_hdim[d];
+    const HaltonDim h = hdim_t<WIDE>(d);
     const uint64_t p = (uint64_t)h.base;
     const int L = h.tdig + 1;
     uint64_t pL = 1;
@@ -877,7 +896,7 @@ struct GenRasrapCounterTile {
   }
   // the point's low L digits, summed from the lowest (sets its variant v)
   __device__ __forceinline__ double low_sum(int rl, int d, int dd, int *v) const {
-    const HaltonDim &h = c_hdim[d];
+    const HaltonDim h = hdim_t<WIDE>(d);
     const uint32_t p = (uint32_t)h.base;
     const int L = h.tdig + 1;
     uint32_t pL = 1;
@@ -1675,33 +1694,31 @@ struct GenKakutaniRuns {
 
 // Tile layout (TILE consecutive paths): at chunk 0 of a tile, thread t
 // advances the orbits of dims t, t + TILE, ... over the tile's paths into
-// the per-CTA scratch [dim][TILE] (doubles); chunks read their columns.
+// the per-CTA scratch [dim][TILE] (doubles); chunks read their columns.  The
+// orbit state of every dim between tiles, xs[dim], follows the CTA's columns
+// in the scratch (any dim up to MAX_DIM; read and written by its own thread).
 struct GenKakutani {
   __device__ void set_dyn(double *) {}
   static __host__ __device__ size_t dyn_bytes(int) { return 0; }
   static constexpr bool RUNS = false;
-  struct Shared {
-    double xs[MAX_DIM];  // orbit state of every dim between tiles
-  };
+  using Shared = NoShared;
   const RepTables *t;
-  Shared *sh;
+  double *xs;
   double *scr;
   const SeqArgs *q;
   int dim;
-  __device__ void setup(const RepTables &t_, Shared &s, uint32_t *) {
-    t = &t_;
-    sh = &s;
-  }
+  __device__ void setup(const RepTables &t_, Shared &, uint32_t *) { t = &t_; }
   __device__ void set_seq(const SeqArgs &q_, int dim_) {
     q = &q_;
     dim = dim_;
-    // this CTA's slice of the scratch, [dim][TILE] doubles
-    scr = reinterpret_cast<double *>(q_.scratch) + (size_t)blockIdx.x * dim_ * TILE;
+    // this CTA's slice of the scratch: [dim][TILE] columns, then xs[dim]
+    scr = reinterpret_cast<double *>(q_.scratch) + (size_t)blockIdx.x * dim_ * (TILE + 1);
+    xs = scr + (size_t)dim_ * TILE;
   }
   __device__ void begin_segment(int, int rb, int sg, int64_t, int64_t, int) {
     const double *src = q->kk_snap + ((int64_t)rb * q->segs_per_rep + sg) * dim;
-    __syncthreads();  // the previous segment's last tile is done with xs
-    for (int d = threadIdx.x; d < dim; d += TILE) sh->xs[d] = src[d];
+    __syncthreads();  // the previous segment's last tile is done with the columns
+    for (int d = threadIdx.x; d < dim; d += TILE) xs[d] = src[d];
   }
   __device__ void skip(int) {}
   __device__ void fill_tile(int npaths) {
@@ -1709,13 +1726,13 @@ struct GenKakutani {
     for (int d = threadIdx.x; d < dim; d += TILE) {
       KakDim kd;
       kd.load(d);
-      double xv = sh->xs[d];
+      double xv = xs[d];
 #pragma unroll 4
       for (int j = 0; j < npaths; j++) {
         scr[d * TILE + j] = xv;
         xv = kd.step(xv);
       }
-      sh->xs[d] = xv;
+      xs[d] = xv;
     }
     __syncthreads();
   }
@@ -1978,6 +1995,58 @@ struct ModelLiborDyn {
     double prod = 1.0;
     for (int n = 0; n < S - 1; n++) prod *= fma(cz, L[n * TILE], 1.0);
     const double lt = L[(S - 1) * TILE];
+    const double pay = fmax(fma(cz, lt, -dstrike), 0.0);
+    return pay * ff * rcp2(fma(cz, lt, 1.0) * prod);
+  }
+};
+
+// LIBOR with S > LIBOR_DYN_MAX steps (up to LIBOR_MAX): ModelLiborDyn's
+// operations in the same order (bit-identical payoffs), the forward rates
+// in a per-CTA slice of global memory, [S][TILE] doubles at
+// mp.lstate + blockIdx.x * S * TILE (coalesced; the launcher sizes the grid
+// to the slices it allocated), and L_n(0) formed from mp.table at begin().
+struct ModelLiborBig {
+  static constexpr bool NORMALS = true;
+  static constexpr bool SMALL_LIBOR = false;
+  static constexpr int MINB = 2;
+  using Shared = NoShared;
+  static __host__ __device__ int gen_dims(int dim) { return dim; }
+  const double *tab;
+  double *Ls;
+  int S;
+  double kz, delta, cz, ssq, dstrike, ff;
+  __device__ void init(const ModelParams &mp_, Shared &) {
+    S = mp_.dim;
+    kz = libor_state_scale(mp_);
+    delta = mp_.delta;
+    tab = mp_.table;
+    Ls = mp_.lstate + (size_t)blockIdx.x * S * TILE + ctid();
+    cz = 1.0 / kz;
+    dstrike = mp_.delta * mp_.strike;
+    ff = mp_.front_factor;
+    ssq = mp_.sigma * sqrt(mp_.delta);
+  }
+  __device__ void begin() {
+    for (int n = 0; n < S; n++) Ls[(size_t)n * TILE] = kz * (delta * tab[n]);
+  }
+  __device__ void chunk(int d0, int Dc, const double *zcol) {
+    for (int k = 0; k < Dc; k++) {
+      const int i = d0 + k;
+      const double g1 = fma(ssq, zcol[k * TILE], 1.0);
+      double f = g1;
+#pragma unroll 4
+      for (int n = i; n < S; n++) {
+        const double ln = Ls[(size_t)n * TILE];
+        const double r = rcp1(fma(cz, ln, 1.0));
+        f = fma(ln, r, f);
+        Ls[(size_t)n * TILE] = ln * f;
+      }
+    }
+  }
+  __device__ double payoff() const {
+    double prod = 1.0;
+    for (int n = 0; n < S - 1; n++) prod *= fma(cz, Ls[(size_t)n * TILE], 1.0);
+    const double lt = Ls[(size_t)(S - 1) * TILE];
     const double pay = fmax(fma(cz, lt, -dstrike), 0.0);
     return pay * ff * rcp2(fma(cz, lt, 1.0) * prod);
   }
@@ -2716,16 +2785,21 @@ __global__ void __launch_bounds__(TILE) k_payoffs_u(ModelParams mp, const double
   md.init(mp, msh);
   ModelDyn<Mdl>::give(md, zt + CHUNK * TILE);
   __syncthreads();
-  int64_t p = (int64_t)blockIdx.x * TILE + threadIdx.x;
-  const bool ok = p < npaths;
-  md.begin();
-  for (int d0 = 0; d0 < mp.dim; d0 += CHUNK) {
-    const int Dc = mp.dim - d0 < CHUNK ? mp.dim - d0 : CHUNK;
-    for (int k = 0; k < Dc; k++)
-      zt[k * TILE + threadIdx.x] = ok ? inv_normal(u[p * mp.dim + d0 + k]) : 0.0;
-    md.chunk(d0, Dc, zt + threadIdx.x);
+  // one tile per CTA; ModelLiborBig: grid-stride (the grid is its state slices)
+  constexpr bool STRIDE = std::is_same<Mdl, ModelLiborBig>::value;
+  for (int64_t p = (int64_t)blockIdx.x * TILE + threadIdx.x; p - threadIdx.x < npaths;
+       p += (int64_t)gridDim.x * TILE) {
+    const bool ok = p < npaths;
+    md.begin();
+    for (int d0 = 0; d0 < mp.dim; d0 += CHUNK) {
+      const int Dc = mp.dim - d0 < CHUNK ? mp.dim - d0 : CHUNK;
+      for (int k = 0; k < Dc; k++)
+        zt[k * TILE + threadIdx.x] = ok ? inv_normal(u[p * mp.dim + d0 + k]) : 0.0;
+      md.chunk(d0, Dc, zt + threadIdx.x);
+    }
+    if (ok) out[p] = md.payoff();
+    if constexpr (!STRIDE) break;
   }
-  if (ok) out[p] = md.payoff();
 }
 
 __global__ void k_inv_normal(const double *u, int64_t n, double *out) {
@@ -2906,11 +2980,15 @@ cudaError_t launch_points(const RepTables &t, int rl, int64_t first, const int64
   const bool at = idx != nullptr;
   switch (t.gen) {
     case GEN_RASRAP_RECURSIVE:
-      return at ? points_t<GenRasrapRecDirect>(t, rl, first, idx, count, out, s)
-                : points_t<GenRasrapRecTile<false>>(t, rl, first, idx, count, out, s);
+      if (at) return points_t<GenRasrapRecDirect>(t, rl, first, idx, count, out, s);
+      return t.dim > CONST_DIMS
+                 ? points_t<GenRasrapRecTile<false, false, true>>(t, rl, first, idx, count, out, s)
+                 : points_t<GenRasrapRecTile<false>>(t, rl, first, idx, count, out, s);
     case GEN_RASRAP_COUNTER:
-      return at ? points_t<GenRasrapCounter>(t, rl, first, idx, count, out, s)
-                : points_t<GenRasrapCounterTile>(t, rl, first, idx, count, out, s);
+      if (at) return points_t<GenRasrapCounter>(t, rl, first, idx, count, out, s);
+      return t.dim > CONST_DIMS
+                 ? points_t<GenRasrapCounterTile<true>>(t, rl, first, idx, count, out, s)
+                 : points_t<GenRasrapCounterTile<false>>(t, rl, first, idx, count, out, s);
     case GEN_PHILOX: return points_t<GenPhilox>(t, rl, first, idx, count, out, s);
     case GEN_SOBOL_GRAY:
       return at ? points_t<GenSobolDirect<true>>(t, rl, first, idx, count, out, s)
@@ -2923,6 +3001,28 @@ cudaError_t launch_points(const RepTables &t, int rl, int64_t first, const int64
   return cudaErrorInvalidValue;
 }
 
+// ModelLiborBig: per-CTA forward-rate state in global memory, allocated in
+// stream order around the launch; the grid is capped so it stays <= 1 GiB
+// (and >= one CTA per SM).
+template <class Mdl>
+static constexpr bool big_libor = std::is_same<Mdl, ModelLiborBig>::value;
+static size_t lstate_bytes(int S) { return sizeof(double) * (size_t)S * TILE; }
+static int lstate_blocks(int64_t blocks, int S) {
+  const int64_t cap = std::max<int64_t>(sm_count(), ((int64_t)1 << 30) / (int64_t)lstate_bytes(S));
+  return (int)std::min<int64_t>(blocks, cap);
+}
+struct LState {
+  double *p = nullptr;
+  cudaStream_t s;
+  explicit LState(cudaStream_t s_) : s(s_) {}
+  cudaError_t alloc(int blocks, int S) {
+    return cudaMallocAsync(reinterpret_cast<void **>(&p), lstate_bytes(S) * blocks, s);
+  }
+  ~LState() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 template <class G, class Mdl>
 static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                             int *blocks_out) {
@@ -2932,7 +3032,8 @@ static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bo
   // never reaches one: GenRasrapCounterTile syncs the whole CTA); RQ_WS = 1:
   // only where it measured faster (the persistent Rasrap tile with LIBOR
   // S <= 20), 2: every eligible pair (experiments)
-  constexpr bool ws_ok = !std::is_same<G, GenRasrapCounterTile>::value;
+  constexpr bool ws_ok = !std::is_same<G, GenRasrapCounterTile<false>>::value &&
+                        !std::is_same<G, GenRasrapCounterTile<true>>::value;
   // (the xhash test integrand takes the same kernel, so its bit-exact theta
   // pins the warp-specialised generator path the C2 headline runs)
   constexpr bool ws_pick = RQ_WS >= 2 || (std::is_same<G, GenRasrapRecTile<true>>::value &&
@@ -2953,9 +3054,19 @@ static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bo
 #endif
   size_t dyn = prep_dyn(k_paths<G, Mdl>, ZT_BYTES + ModelDyn<Mdl>::bytes(a.mp.dim));
   int blocks = persistent_blocks(k_paths<G, Mdl>, work, dyn);
+  if constexpr (big_libor<Mdl>) blocks = lstate_blocks(blocks, a.mp.dim);
   if (blocks_out) *blocks_out = blocks;
   if (probe) return cudaSuccess;
-  k_paths<G, Mdl><<<blocks, TILE, dyn, s>>>(a);
+  if constexpr (big_libor<Mdl>) {
+    LState ls(s);
+    cudaError_t e = ls.alloc(blocks, a.mp.dim);
+    if (e != cudaSuccess) return e;
+    PathArgs b = a;
+    b.mp.lstate = ls.p;
+    k_paths<G, Mdl><<<blocks, TILE, dyn, s>>>(b);
+  } else {
+    k_paths<G, Mdl><<<blocks, TILE, dyn, s>>>(a);
+  }
   if (launched) *launched += 1;
   return cudaGetLastError();
 }
@@ -2973,6 +3084,28 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
       }
       if (a.mp.dim >= 1 && a.mp.dim <= LIBOR_DYN_MAX)
         return paths_gm<G, ModelLiborDyn>(a, launched, s, probe, blocks);
+      if (a.mp.dim > LIBOR_DYN_MAX && a.mp.dim <= LIBOR_MAX)
+        return paths_gm<G, ModelLiborBig>(a, launched, s, probe, blocks);
+      return cudaErrorInvalidValue;
+    case MODEL_MBS:
+      if (a.mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
+      return paths_gm<G, ModelMbs>(a, launched, s, probe, blocks);
+    case MODEL_X1: return paths_gm<G, ModelTest<false>>(a, launched, s, probe, blocks);
+    case MODEL_CONST1: return paths_gm<G, ModelTest<true>>(a, launched, s, probe, blocks);
+    case MODEL_XHASH: return paths_gm<G, ModelHash>(a, launched, s, probe, blocks);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// generators of more than CONST_DIMS dims: only the models that take that
+// many (LIBOR past the shared-memory model, MBS, the test integrands)
+template <class G>
+static cudaError_t paths_g_wide(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
+                                int *blocks) {
+  switch (a.mp.kind) {
+    case MODEL_LIBOR:
+      if (a.mp.dim > LIBOR_DYN_MAX && a.mp.dim <= LIBOR_MAX)
+        return paths_gm<G, ModelLiborBig>(a, launched, s, probe, blocks);
       return cudaErrorInvalidValue;
     case MODEL_MBS:
       if (a.mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
@@ -2988,10 +3121,15 @@ static cudaError_t paths_dispatch(const PathArgs &a, int *launched, cudaStream_t
                                   int *blocks) {
   switch (a.t.gen) {
     case GEN_RASRAP_RECURSIVE:
+      if (a.t.dim > CONST_DIMS)
+        return paths_g_wide<GenRasrapRecTile<false, false, true>>(a, launched, s, probe, blocks);
       return a.mp.kind == MODEL_MBS || a.mp.dim > CHUNK
                  ? paths_g<GenRasrapRecTile<false>>(a, launched, s, probe, blocks)
                  : paths_g<GenRasrapRecTile<true>>(a, launched, s, probe, blocks);
-    case GEN_RASRAP_COUNTER: return paths_g<GenRasrapCounterTile>(a, launched, s, probe, blocks);
+    case GEN_RASRAP_COUNTER:
+      if (a.t.dim > CONST_DIMS)
+        return paths_g_wide<GenRasrapCounterTile<true>>(a, launched, s, probe, blocks);
+      return paths_g<GenRasrapCounterTile<false>>(a, launched, s, probe, blocks);
     case GEN_PHILOX: return paths_g<GenPhilox>(a, launched, s, probe, blocks);
 #if RQ_SOBOL_PERSIST
     case GEN_SOBOL_GRAY:
@@ -3076,9 +3214,21 @@ static cudaError_t seq_gm(const PathArgs &a, const SeqArgs &q, int blocks, int *
   if (occ) {
     *occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_paths_seq<G, Mdl>, TILE, dyn);
+    if constexpr (big_libor<Mdl>)  // seq_layout's CTA count, capped to the rate-state slices
+      *occ = std::max(1, std::min(*occ, lstate_blocks((int64_t)*occ * sm_count(), a.mp.dim) /
+                                            sm_count()));
     return cudaSuccess;
   }
-  k_paths_seq<G, Mdl><<<blocks, TILE, dyn, s>>>(a, q);
+  if constexpr (big_libor<Mdl>) {
+    LState ls(s);
+    cudaError_t e = ls.alloc(blocks, a.mp.dim);
+    if (e != cudaSuccess) return e;
+    PathArgs b = a;
+    b.mp.lstate = ls.p;
+    k_paths_seq<G, Mdl><<<blocks, TILE, dyn, s>>>(b, q);
+  } else {
+    k_paths_seq<G, Mdl><<<blocks, TILE, dyn, s>>>(a, q);
+  }
   if (launched) *launched += 1;
   return cudaGetLastError();
 }
@@ -3096,6 +3246,8 @@ static cudaError_t seq_g(const PathArgs &a, const SeqArgs &q, int blocks, int *l
       }
       if (a.mp.dim >= 1 && a.mp.dim <= LIBOR_DYN_MAX)
         return seq_gm<G, ModelLiborDyn>(a, q, blocks, launched, s, occ);
+      if (a.mp.dim > LIBOR_DYN_MAX && a.mp.dim <= LIBOR_MAX)
+        return seq_gm<G, ModelLiborBig>(a, q, blocks, launched, s, occ);
       return cudaErrorInvalidValue;
     case MODEL_MBS:
       if (a.mp.dim > ModelMbs::MAXM) return cudaErrorInvalidValue;
@@ -3191,6 +3343,16 @@ cudaError_t launch_model_payoffs(const ModelParams &mp, const double *u, int64_t
       break;
     }
     default: {
+      if (mp.dim > LIBOR_DYN_MAX && mp.dim <= LIBOR_MAX) {
+        const int nb = lstate_blocks(blocks, mp.dim);
+        LState ls(s);
+        cudaError_t e = ls.alloc(nb, mp.dim);
+        if (e != cudaSuccess) return e;
+        ModelParams m2 = mp;
+        m2.lstate = ls.p;
+        k_payoffs_u<ModelLiborBig><<<nb, TILE, ZT_BYTES, s>>>(m2, u, npaths, out);
+        break;
+      }
       if (mp.dim < 1 || mp.dim > LIBOR_DYN_MAX) return cudaErrorInvalidValue;
       const size_t dyn =
           prep_dyn(k_payoffs_u<ModelLiborDyn>, ZT_BYTES + ModelDyn<ModelLiborDyn>::bytes(mp.dim));
@@ -3246,7 +3408,7 @@ int stream_grid_blocks(const RepTables &t) {
                                         GenSobolStream<false>::dyn_bytes(t.dim)));
 #endif
     case GEN_RASRAP_RECURSIVE: {  // chunk-major
-      using K = GenRasrapRecTile<true, false>;
+      using K = GenRasrapRecTile<true, false>;  // (the WIDE form has the same footprint)
       return persistent_blocks(k_stream_chunks<K>, big, prep_dyn(k_stream_chunks<K>, ZT_BYTES));
     }
   }
@@ -3256,32 +3418,44 @@ int stream_grid_blocks(const RepTables &t) {
   return paths_grid_blocks(t, mp);
 }
 
+// chunk-major Rasrap stream (per-chunk run counters, zeroed in stream order)
+template <class K>
+static cudaError_t stream_chunks_t(const RepTables &t, int rl, int64_t npoints, double *block_sums,
+                                   int nblocks, double *store, cudaStream_t s) {
+  const int nchunk = (t.dim + CHUNK - 1) / CHUNK;
+  unsigned long long *ctr = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long) * nchunk, s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * nchunk, s);
+  if (store) {
+    prep_dyn(k_stream_chunks<K, true>, ZT_BYTES);
+    k_stream_chunks<K, true><<<nblocks, TILE, ZT_BYTES, s>>>(t, rl, npoints, block_sums, store,
+                                                             ctr);
+  } else {
+    prep_dyn(k_stream_chunks<K, false>, ZT_BYTES);
+    k_stream_chunks<K, false><<<nblocks, TILE, ZT_BYTES, s>>>(t, rl, npoints, block_sums,
+                                                              nullptr, ctr);
+  }
+  e = cudaGetLastError();
+  cudaFreeAsync(ctr, s);
+  return e;
+}
+
 cudaError_t launch_stream_normals(const RepTables &t, int rl, int64_t npoints,
                                   double *block_sums, int nblocks, double *store,
                                   cudaStream_t s) {
   switch (t.gen) {
-    case GEN_RASRAP_RECURSIVE: {
-      using K = GenRasrapRecTile<true, false>;
-      const int nchunk = (t.dim + CHUNK - 1) / CHUNK;
-      unsigned long long *ctr = nullptr;
-      cudaError_t e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long) * nchunk, s);
-      if (e != cudaSuccess) return e;
-      cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * nchunk, s);
-      if (store) {
-        prep_dyn(k_stream_chunks<K, true>, ZT_BYTES);
-        k_stream_chunks<K, true><<<nblocks, TILE, ZT_BYTES, s>>>(t, rl, npoints, block_sums,
-                                                                 store, ctr);
-      } else {
-        prep_dyn(k_stream_chunks<K, false>, ZT_BYTES);
-        k_stream_chunks<K, false><<<nblocks, TILE, ZT_BYTES, s>>>(t, rl, npoints, block_sums,
-                                                                  nullptr, ctr);
-      }
-      e = cudaGetLastError();
-      cudaFreeAsync(ctr, s);
-      return e;
-    }
+    case GEN_RASRAP_RECURSIVE:
+      return t.dim > CONST_DIMS
+                 ? stream_chunks_t<GenRasrapRecTile<true, false, true>>(t, rl, npoints, block_sums,
+                                                                        nblocks, store, s)
+                 : stream_chunks_t<GenRasrapRecTile<true, false>>(t, rl, npoints, block_sums,
+                                                                  nblocks, store, s);
     case GEN_RASRAP_COUNTER:
-      return stream_t<GenRasrapCounterTile>(t, rl, npoints, block_sums, nblocks, store, s);
+      return t.dim > CONST_DIMS
+                 ? stream_t<GenRasrapCounterTile<true>>(t, rl, npoints, block_sums, nblocks, store, s)
+                 : stream_t<GenRasrapCounterTile<false>>(t, rl, npoints, block_sums, nblocks, store,
+                                                         s);
     case GEN_PHILOX: return stream_reg_t<GenPhilox>(t, rl, npoints, block_sums, nblocks, store, s);
 #if RQ_SOBOL_STREAM_REG
     case GEN_SOBOL_GRAY:

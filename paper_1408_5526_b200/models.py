@@ -134,8 +134,11 @@ def init_libor(bonds: np.ndarray, accrual: float) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- LIBOR
-LIBOR_STEPS = (10, 20, 40, 80)  # register-resident path kernels (others: shared-memory model)
-LIBOR_MAX_STEPS = 160
+LIBOR_STEPS = (10, 20, 40, 80)  # register-resident path kernels
+# others: forward rates in shared memory up to 160 steps, in a per-CTA slice
+# of global memory beyond (the reference takes any count, models.py:172-193;
+# the cap is the Halton dimension cap, every base below 2^16)
+LIBOR_MAX_STEPS = 6542
 
 
 @dataclass(frozen=True)

@@ -285,6 +285,68 @@ def _section_kak(out, versions, H, M, prng, seeding):
     np.savez_compressed(out / "kakutani.npz", **z)
 
 
+BIG_COLS_STEP = 97
+LONG_CURVE = ((0.25, 1.0, 2.0, 5.0, 10.0, 30.0, 60.0, 100.0, 160.0),
+              (1.0, 1.2, 1.5, 2.0, 2.5, 3.0, 3.2, 3.3, 3.4))  # tenor years, rate percent
+
+
+def _big_cols(dim: int) -> np.ndarray:
+    """Columns kept of a wide row: the first and last 24, the constant-bank
+    edge (512), and every BIG_COLS_STEP-th."""
+    cols = set(range(min(24, dim))) | set(range(max(0, dim - 24), dim))
+    cols |= {c for c in range(500, 530) if c < dim} | set(range(0, dim, BIG_COLS_STEP))
+    return np.array(sorted(cols), dtype=np.int64)
+
+
+def _section_bigdim(out, versions, H, M, prng, seeding):
+    """Dimensions beyond the first 512 primes (up to every base < 2^16) and
+    LIBOR beyond 160 steps: points of the reference's own samplers (selected
+    columns) and per-replication estimates."""
+    import time
+
+    z = {"versions": versions}
+    for gen, dim, m in (("rasrap", 6542, 1), ("rasrap", 1000, 2), ("kakutani", 700, 1)):
+        tag = f"{gen}_d{dim}_m{m}"
+        cols = _big_cols(dim)
+        z[f"{tag}_cols"] = cols
+        t0 = time.time()
+        if gen == "rasrap":
+            rows = np.arange(300, dtype=np.int64)
+            z[f"{tag}_recursive"] = _fill_rows(H.make_sampler("rasrap-recursive", dim, SEED, m),
+                                               dim, 300, rows)[:, cols]
+            idx = np.array([0, 1, 127, 128, 300, 12345, 2**20 + 3, 2**32 + 7, 3 * 2**33 + 5],
+                           dtype=np.int64)
+            z[f"{tag}_idx"] = idx
+            z[f"{tag}_counter"] = H.make_sampler("rasrap-counter", dim, SEED, m).at(idx)[:, cols]
+        else:
+            rows = _rows(3000, head=300, step=997)
+            z[f"{tag}_rows"] = rows
+            z[f"{tag}_points"] = _fill_rows(H.make_sampler(gen, dim, SEED, m), dim, 3000,
+                                            rows)[:, cols]
+        print(tag, f"{time.time() - t0:.1f}s", flush=True)
+    # 200 steps on the default curve (it ends at 30 years); 600 on a longer
+    # user curve (YieldCurve takes any tenors, models.py:96-112)
+    s200 = M.LiborModel(M.LiborConfig(maturity=25.0, accrual=0.125))
+    z["long_curve"] = np.array([LONG_CURVE[0], LONG_CURVE[1]])
+    s600 = M.LiborModel(M.LiborConfig(maturity=150.0, accrual=0.25),
+                        curve=M.YieldCurve(np.array(LONG_CURVE[0]), np.array(LONG_CURVE[1])))
+    for tag, mname, gen, grid, reps, model in (
+            ("libor200_rasrap", "libor", "rasrap-recursive", (300, 1000), 2, s200),
+            ("libor200_philox", "libor", "philox", (1000,), 2, s200),
+            ("libor600_rasrap", "libor", "rasrap-recursive", (257,), 2, s600),
+            ("libor600_counter", "libor", "rasrap-counter", (257,), 2, s600),
+            ("mbs600_rasrap", "mbs", "rasrap-recursive", (500,), 2, M.MbsModel(M.MbsConfig(months=600))),
+            ("libor200_kakutani", "libor", "kakutani", (500,), 2, s200)):
+        t0 = time.time()
+        cfg = H.ExperimentConfig(model=mname, generator=gen, n_grid=grid, replications=reps,
+                                 seed=SEED, workers=2)
+        rep = H.run_experiment(cfg, model=model)
+        z[f"{tag}_grid"] = np.array(grid, dtype=np.int64)
+        z[f"{tag}_theta"] = np.stack([rep.estimates(gen, n) for n in grid])
+        print(tag, z[f"{tag}_theta"][:, 0], f"{time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(out / "bigdim.npz", **z)
+
+
 def _words(gen, n: int) -> np.ndarray:
     w = np.empty(n, dtype=np.uint32)
     gen.fill_words(w)

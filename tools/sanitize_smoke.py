@@ -63,6 +63,19 @@ for gen in COUNTER:
         torch.cuda.synchronize()
         s.close()
 
+# dims past the constant bank (global HaltonDim / Kakutani state) and LIBOR
+# past the shared-memory model (per-CTA rate state in global memory)
+for gen in ("rasrap-recursive", "rasrap-counter", "kakutani"):
+    s = DeviceSampler(gen, 600, SEED, 1)
+    s.points(0, 130)
+    torch.cuda.synchronize()
+    s.close()
+big = M.LiborModel(M.LiborConfig(maturity=25.0, accrual=0.125))
+for gen in ("rasrap-recursive", "philox", "xorwow"):
+    th = estimate_replications(gen, big, SEED, 1, 2, (300,))
+    assert np.all(np.isfinite(th)), gen
+big.payoffs(np.random.default_rng(2).random((300, big.dim)))
+
 # model payoffs and the scalar inverse normal from caller uniforms
 u = np.random.default_rng(1).random((257, 20))
 M.LiborModel(M.LiborConfig(maturity=5.0, accrual=0.25)).payoffs(u)
