@@ -1871,7 +1871,7 @@ __device__ __forceinline__ double libor_state_scale(const ModelParams &mp) {
 // deflator prod (1 + delta L_i(T_i)) is formed as a product and inverted
 // once (each L_i is frozen after step i, so its final value is its fixing,
 // models.py:289-290).
-template <int S>
+template <int S, int NSR = RQ_LIBOR_SMEM_RATES>
 struct ModelLibor {
   static constexpr bool NORMALS = true;
   static constexpr bool SMALL_LIBOR = S <= 20;
@@ -1886,7 +1886,7 @@ struct ModelLibor {
   // (they die first: step i only touches rates n >= i), the rest in
   // registers, so a thread needs ~100 fewer registers and three CTAs fit an
   // SM instead of two.
-  static constexpr int NS = S >= 80 ? RQ_LIBOR_SMEM_RATES : 0;
+  static constexpr int NS = S >= 80 ? NSR : 0;
   static __host__ __device__ size_t dyn_bytes(int) { return sizeof(double) * NS * TILE; }
   const Shared *sh;
   double *Ls;
@@ -3108,6 +3108,19 @@ static cudaError_t paths_gm(const PathArgs &a, int *launched, cudaStream_t s, bo
   return cudaGetLastError();
 }
 
+// LIBOR S = 80 in the fused kernel: 24 of the rates in shared memory (fewer
+// shared-memory round trips than 40 at the same 3 CTAs/SM: +3.7% C5 Rasrap,
+// +2.4% Philox); the counter-form tile needs more registers of its own and
+// keeps 40 (24 spills there).
+template <class G>
+struct LiborSmemRates {
+  static constexpr int value = 24;
+};
+template <bool W>
+struct LiborSmemRates<GenRasrapCounterTile<W>> {
+  static constexpr int value = RQ_LIBOR_SMEM_RATES;
+};
+
 template <class G>
 static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, bool probe,
                            int *blocks) {
@@ -3117,7 +3130,8 @@ static cudaError_t paths_g(const PathArgs &a, int *launched, cudaStream_t s, boo
         case 10: return paths_gm<G, ModelLibor<10>>(a, launched, s, probe, blocks);
         case 20: return paths_gm<G, ModelLibor<20>>(a, launched, s, probe, blocks);
         case 40: return paths_gm<G, ModelLibor<40>>(a, launched, s, probe, blocks);
-        case 80: return paths_gm<G, ModelLibor<80>>(a, launched, s, probe, blocks);
+        case 80: return paths_gm<G, ModelLibor<80, LiborSmemRates<G>::value>>(a, launched, s, probe,
+                                                                             blocks);
       }
       if (a.mp.dim >= 1 && a.mp.dim <= LIBOR_DYN_MAX)
         return paths_gm<G, ModelLiborDyn>(a, launched, s, probe, blocks);
