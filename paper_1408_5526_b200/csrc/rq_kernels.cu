@@ -2660,7 +2660,10 @@ __global__ void __launch_bounds__(TILE, 4) k_stream(RepTables t, int rl, int64_t
 #endif
 constexpr int STREAM_RUN = RQ_STREAM_RUN;  // tiles per counter grab
 template <class G, bool STORE = true>
-__global__ void __launch_bounds__(TILE, 4) k_stream_chunks(RepTables t, int rl, int64_t npoints,
+#ifndef RQ_STREAM_MINB
+#define RQ_STREAM_MINB 5  // (4: -2.3% C4 Rasrap, 6: -6.5%)
+#endif
+__global__ void __launch_bounds__(TILE, RQ_STREAM_MINB) k_stream_chunks(RepTables t, int rl, int64_t npoints,
                                                            double *block_sums, double *store,
                                                            unsigned long long *ctr) {
   extern __shared__ __align__(16) double zt[];  // ZT_BYTES
