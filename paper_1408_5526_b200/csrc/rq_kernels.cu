@@ -63,6 +63,9 @@
 #ifndef RQ_G2_FAST
 #define RQ_G2_FAST 1  // global-sigma Rasrap tiles: level-pass-free path for J == 1 / small J == 2
 #endif
+#ifndef RQ_CT_CACHE
+#define RQ_CT_CACHE 1  // counter-form tile: high-term tables reused while the prefix H0 is unchanged
+#endif
 #ifndef RQ_CT_PAIRS
 #define RQ_CT_PAIRS 1  // counter-form tile: two dims' sum chains per thread at a time
                        // (+2.4% C2, +3.4% C3, +8.2% C4 rasrap-counter; four: -4% C2)
@@ -848,12 +851,18 @@ struct GenRasrapCounterTile {
     double T[CHUNK][2][CT_MAXT];
     int32_t nT[CHUNK][2];
     uint32_t lowB[CHUNK];
+    // (replication, dim, H0) the slot's T tables were formed for: a CTA's
+    // consecutive tiles share H0 for p^L / TILE tiles, so the high terms are
+    // formed once per prefix, not per tile (single-chunk models)
+    int32_t c_rl[CHUNK], c_d[CHUNK];
+    uint64_t c_h[CHUNK];
   };
   const RepTables *t;
   Shared *sh;
   __device__ void setup(const RepTables &t_, Shared &s, int = 0) {
     t = &t_;
     sh = &s;
+    for (int k = threadIdx.x; k < CHUNK; k += TILE) s.c_rl[k] = -1;
   }
   __device__ void prepare(int rl, uint64_t base, int d, int dd) {  // one lane per dim
     const HaltonDim h = hdim_t<WIDE>(d);
@@ -864,6 +873,12 @@ struct GenRasrapCounterTile {
     const uint64_t B = t->start[(int64_t)rl * t->dim + d] + base;
     const uint64_t H0 = B / pL;
     sh->lowB[dd] = (uint32_t)(B - H0 * pL);
+#if RQ_CT_CACHE
+    if (sh->c_rl[dd] == rl && sh->c_d[dd] == d && sh->c_h[dd] == H0) return;
+    sh->c_rl[dd] = rl;
+    sh->c_d[dd] = d;
+    sh->c_h[dd] = H0;
+#endif
     const uint16_t *sg = t->sigma + (int64_t)rl * t->sig_stride + h.sig_off;
     const double *cs = g_cscale + h.sum_off;
 #pragma unroll 1
