@@ -608,7 +608,9 @@ int rq_sampler_create(rq_sampler **out, int generator, int dim, uint64_t seed,
     t.start = start;
     {
       KTimer kt(&g_stats.setup_ms, s);
-      e = rq::launch_rasrap_setup(t, sig, dig, sums, start, s);
+      std::vector<int> bases(dim);
+      for (int d = 0; d < dim; d++) bases[d] = T.dims[d].base;
+      e = rq::launch_rasrap_setup(t, sig, dig, sums, start, s, bases.data());
     }
     if (e != cudaSuccess) {
       cudaFreeAsync(S->mem, s);

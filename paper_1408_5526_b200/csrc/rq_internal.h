@@ -139,7 +139,8 @@ struct SumPlan {
 cudaError_t upload_halton_dims(const HaltonDim *dims, int n, const double *wts,
                                const double *cscale, int nw);
 cudaError_t launch_rasrap_setup(const RepTables &t, uint16_t *sigma, uint16_t *digits,
-                                double *sums, uint64_t *start, cudaStream_t s);
+                                double *sums, uint64_t *start, cudaStream_t s,
+                                const int *bases);  // host: the dims' bases
 cudaError_t launch_sobol_setup(const RepTables &t, const uint32_t *v_dev, uint32_t *gen_v,
                                uint32_t *shift, cudaStream_t s);
 cudaError_t launch_points(const RepTables &t, int rep_local, int64_t first,

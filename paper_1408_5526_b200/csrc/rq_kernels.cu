@@ -155,25 +155,12 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
 
 // One thread per (replication, dimension): rasrap_config + RasrapStream
 // init (halton.py:345-360, 256-278, 139-155; seeding.py:59-65).
-__global__ void k_rasrap_setup(RepTables t, uint16_t *sigma, uint16_t *digits, double *sums,
-                               uint64_t *start) {
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)t.rep_count * t.dim) return;
-  int rl = (int)(gid / t.dim), d = (int)(gid % t.dim);
-  const HaltonDim h = hdim(d);
-  uint64_t m = (uint64_t)(t.rep_first + rl);
-  uint64_t key = derive_key3(t.seed, 4, m);  // harness.py:113, family "rasrap"
-  Pcg64 g;
-  pcg_seed(g, derive_key2(key, (uint64_t)d));  // derive_rng(seed, i)
-  uint64_t k53 = pcg_next64(g) >> 11;          // rng.random() = k53 * 2^-53
-  uint16_t *sg = sigma + (int64_t)rl * t.sig_stride + h.sig_off;
-  for (int a = 0; a < h.base; a++) sg[a] = (uint16_t)a;
-  for (int i = h.base - 1; i >= 1; i--) {  // rng.permutation(p)
-    int j = (int)pcg_interval32(g, (uint32_t)i);
-    uint16_t tmp = sg[j];
-    sg[j] = sg[i];
-    sg[i] = tmp;
-  }
+// invert_radical (start digits, n0) and the init partial sums of one
+// (replication, dim) from its permutation sg (halton.py:139-155, 273-278)
+template <class SG>
+__device__ void rasrap_start_and_sums(const RepTables &t, int rl, int d, const HaltonDim &h,
+                                      uint64_t k53, SG sgv, uint16_t *digits, double *sums,
+                                      uint64_t *start) {
   // invert_radical: scaled = floor(k53 * p^K / 2^53), digits reversed
   uint64_t pk = 1;
   for (int i = 0; i < h.K; i++) pk *= (uint64_t)h.base;
@@ -194,9 +181,70 @@ __global__ void k_rasrap_setup(RepTables t, uint16_t *sigma, uint16_t *digits, d
   for (int j = h.K; j <= h.cap; j++) sm[j] = 0.0;
   double scale = h.scale0;
   for (int j = h.K - 1; j >= 0; j--) {
-    sm[j] = dadd(sm[j + 1], dmul((double)sg[dg[j]], scale));
+    sm[j] = dadd(sm[j + 1], dmul((double)sgv(dg[j]), scale));
     scale = dmul(scale, (double)h.base);
   }
+}
+
+// One thread per (replication, dim) of dims [d_lo, d_hi) (small bases: short
+// shuffles).  derive_rng(key, d).random() then .permutation(p).
+__global__ void k_rasrap_setup(RepTables t, int d_lo, int d_hi, uint16_t *sigma,
+                               uint16_t *digits, double *sums, uint64_t *start) {
+  const int nd = d_hi - d_lo;
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)t.rep_count * nd) return;
+  int rl = (int)(gid / nd), d = d_lo + (int)(gid % nd);
+  const HaltonDim h = hdim(d);
+  uint64_t m = (uint64_t)(t.rep_first + rl);
+  uint64_t key = derive_key3(t.seed, 4, m);  // harness.py:113, family "rasrap"
+  Pcg64 g;
+  pcg_seed(g, derive_key2(key, (uint64_t)d));  // derive_rng(seed, i)
+  uint64_t k53 = pcg_next64(g) >> 11;          // rng.random() = k53 * 2^-53
+  uint16_t *sg = sigma + (int64_t)rl * t.sig_stride + h.sig_off;
+  for (int a = 0; a < h.base; a++) sg[a] = (uint16_t)a;
+  for (int i = h.base - 1; i >= 1; i--) {  // rng.permutation(p)
+    int j = (int)pcg_interval32(g, (uint32_t)i);
+    uint16_t tmp = sg[j];
+    sg[j] = sg[i];
+    sg[i] = tmp;
+  }
+  rasrap_start_and_sums(t, rl, d, h, k53, [&](uint32_t a) { return sg[a]; }, digits, sums, start);
+}
+
+// One warp per (replication, dim) of dims [d_lo, d_hi) (large bases): the
+// shuffle is one sequential chain of p draws and swaps, so it runs on lane 0
+// against a shared-memory copy (30-cycle instead of L2-latency swaps); the
+// lanes initialise and write the permutation out coalesced.
+__global__ void k_rasrap_setup_warp(RepTables t, int d_lo, int d_hi, int smax, uint16_t *sigma,
+                                    uint16_t *digits, double *sums, uint64_t *start) {
+  extern __shared__ uint16_t perm_sm[];
+  const int nd = d_hi - d_lo, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t unit = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (unit >= (int64_t)t.rep_count * nd) return;
+  const int rl = (int)(unit / nd), d = d_lo + (int)(unit % nd);
+  const HaltonDim h = hdim(d);
+  uint16_t *ps = perm_sm + (size_t)w * smax;
+  for (int a = lane; a < h.base; a += 32) ps[a] = (uint16_t)a;
+  __syncwarp();
+  uint64_t k53 = 0;
+  if (lane == 0) {
+    uint64_t key = derive_key3(t.seed, 4, (uint64_t)(t.rep_first + rl));
+    Pcg64 g;
+    pcg_seed(g, derive_key2(key, (uint64_t)d));
+    k53 = pcg_next64(g) >> 11;
+    for (int i = h.base - 1; i >= 1; i--) {
+      int j = (int)pcg_interval32(g, (uint32_t)i);
+      uint16_t tmp = ps[j];
+      ps[j] = ps[i];
+      ps[i] = tmp;
+    }
+  }
+  __syncwarp();
+  uint16_t *sg = sigma + (int64_t)rl * t.sig_stride + h.sig_off;
+  for (int a = lane; a < h.base; a += 32) sg[a] = ps[a];
+  if (lane == 0)
+    rasrap_start_and_sums(t, rl, d, h, k53, [&](uint32_t a) { return ps[a]; }, digits, sums,
+                          start);
 }
 
 // One thread per (replication, dimension): random_scramble + pre-scrambled
@@ -3004,11 +3052,33 @@ cudaError_t launch_dfma_peak(int blocks, int iters, double *sink, cudaStream_t s
   return cudaGetLastError();
 }
 
+// Few (replication, dim) units with large bases (a single replication of a
+// wide sampler, the config-4 stream): the setup is the latency of the
+// longest shuffle chain, so those units get a warp each and shuffle in
+// shared memory.  Many units (replication groups): one thread per unit
+// keeps 32 chains in flight per warp, which wins on throughput.
+constexpr int SETUP_WARP_P = 256, SETUP_WARP_PMAX = 8192, SETUP_WARP_UNITS = 16384;
 cudaError_t launch_rasrap_setup(const RepTables &t, uint16_t *sigma, uint16_t *digits,
-                                double *sums, uint64_t *start, cudaStream_t s) {
-  int64_t n = (int64_t)t.rep_count * t.dim;
-  int blocks = (int)((n + 127) / 128);
-  k_rasrap_setup<<<blocks, 128, 0, s>>>(t, sigma, digits, sums, start);
+                                double *sums, uint64_t *start, cudaStream_t s,
+                                const int *bases) {
+  int dsplit = 0;
+  while (dsplit < t.dim && bases[dsplit] <= SETUP_WARP_P) dsplit++;
+  const int64_t big_units = (int64_t)t.rep_count * (t.dim - dsplit);
+  if (big_units == 0 || big_units > SETUP_WARP_UNITS || bases[t.dim - 1] > SETUP_WARP_PMAX)
+    dsplit = t.dim;
+  {
+    const int64_t n = (int64_t)t.rep_count * dsplit;
+    if (n > 0)
+      k_rasrap_setup<<<(int)((n + 127) / 128), 128, 0, s>>>(t, 0, dsplit, sigma, digits, sums,
+                                                            start);
+  }
+  if (dsplit < t.dim) {
+    const int smax = (bases[t.dim - 1] + 7) & ~7;  // u16 entries per warp (<= 16 KB)
+    const int wpb = std::max(1, std::min(8, (48 << 10) / (2 * smax)));
+    k_rasrap_setup_warp<<<(int)((big_units + wpb - 1) / wpb), 32 * wpb,
+                          (size_t)wpb * smax * 2, s>>>(t, dsplit, t.dim, smax, sigma, digits, sums,
+                                                       start);
+  }
   return cudaGetLastError();
 }
 
